@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""Benchmark of the ESC SpMM hot path (arXiv 2506.15174) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl escs|reference]
+                    [--workload transformer|resnet|suite|c1|c4|c5] [--no-compare]
+
+A *step* is one pass of the whole hot path over the workload: one
+``escs_spmm`` (one kernel launch) per problem of the workload with inputs
+resident in HBM.  Default workload (N=1): configs[1] of BASELINE.json, the
+sparse-Transformer suite {512x512, 2048x512, 512x2048} x {70,80,90,95,98}%
+x bCols {32,64,128} = 45 SpMMs per step.  With N>1 ranks (torchrun), every
+problem is row-block sharded (rank r owns rows [r*m/N, (r+1)*m/N), B
+replicated, no collective on the hot path): total work is
+fixed, so scaling is "strong".
+
+Timing: W untimed warm-up steps, then K timed steps.  Before each step the L2
+is flushed by writing a 256 MiB buffer (> 126 MB L2), and a device-side sleep
+is queued so that the host enqueues the whole step ahead of the GPU; the step
+itself is bracketed by CUDA events on the launching stream (flush and sleep
+are outside the events).  Barrier + synchronize on both sides; max over ranks.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
+(fp64, oracle/) on the same workload instead (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMM GFLOP/s and % HBM roofline, geomean speedup vs cuSPARSE/cuBLAS, bCols 32–128"
+UNIT = "GFLOP/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)", d
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
+
+
+def workload(name):
+    from paper_2506_15174_b200 import synth
+    if name == "transformer":
+        return synth.transformer_suite(), "configs[1]: sparse Transformer 512x512/2048x512/512x2048 x 70-98% x bCols 32/64/128"
+    if name == "resnet":
+        return synth.resnet_suite(), "configs[2]: ResNet-50 im2col 256x2304/512x4608/2048x512 x 70-98% x bCols 32/64/128"
+    if name == "suite":
+        return synth.suite(), "configs[1]+[2]: Transformer + ResNet-50 suites x bCols 32/64/128"
+    if name in ("c1", "c4", "c5"):
+        p = synth.config(name)
+        return [p], p.name
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+            self.t.join(1)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def oracle_time(problems, budget_s=8.0, max_reps=50):
+    """Time the fp64 CPU oracle over the whole workload (repeated until about
+    budget_s of CPU work).  Returns (GFLOP/s, reps, seconds, threads)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    flops = sum(p.flops for p in problems)
+    reps, t_total = 0, 0.0
+    while reps < max_reps and t_total < budget_s:
+        t0 = time.perf_counter()
+        for p in problems:
+            A = p.A
+            oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, p.B, nthreads=threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return flops * reps / t_total / 1e9, reps, t_total, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    import oracle
+    problems, desc = workload(args.workload)
+    threads = os.cpu_count() or 1
+    flops = sum(p.flops for p in problems)
+    for _ in range(args.warmup):
+        for p in problems:
+            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        for p in problems:
+            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, nthreads=threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = flops * args.steps / tot / 1e9
+    sample = f"whole workload ({len(problems)} SpMMs) per step, fp64 C oracle, OpenMP over rows"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": desc, "problems": len(problems)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- escs arm
+
+def geomean(xs):
+    xs = [x for x in xs if x and x > 0 and math.isfinite(x)]
+    return math.exp(sum(math.log(x) for x in xs) / len(xs)) if xs else None
+
+
+def graph_time(torch, fn, stream, min_ms=2.0, reps=11):
+    """Per-call time of fn (enqueue-only) with a CUDA graph of R calls,
+    replayed `reps` times (hot L2, the paper's warm-cache protocol P:675)."""
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(10):
+        with torch.cuda.stream(stream):
+            fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    t1 = s.elapsed_time(e) / 10
+    R = int(min(1000, max(10, math.ceil(min_ms / max(t1, 1e-4)))))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(R):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        s.record(stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+        e.record(stream)
+        e.synchronize()
+        ts.append(s.elapsed_time(e) / R)
+    del g
+    return statistics.median(ts)
+
+
+def compare_baselines(torch, problems, dev, stream):
+    """Per-case hot-L2 times for escs, cuSPARSE (best of 4 algorithms),
+    cuBLAS fp32 and cuBLAS TF32 (context), same inputs, same protocol."""
+    import ctypes
+    from paper_2506_15174_b200 import escs
+    from paper_2506_15174_b200.build import BENCH_LIB
+    bl = ctypes.CDLL(BENCH_LIB)
+    vp = ctypes.c_void_p
+    bl.bl_cusparse_create.restype = vp
+    bl.bl_cusparse_create.argtypes = [ctypes.c_int] * 4 + [vp] * 5 + [ctypes.c_int, vp]
+    bl.bl_cusparse_run.argtypes = [vp, vp]
+    bl.bl_cusparse_destroy.argtypes = [vp]
+    bl.bl_cublas_create.restype = vp
+    bl.bl_cublas_sgemm.argtypes = [vp] + [ctypes.c_int] * 3 + [vp] * 3 + [ctypes.c_int, vp]
+    bl.bl_cublas_destroy.argtypes = [vp]
+    cub = bl.bl_cublas_create()
+    sp = stream.cuda_stream
+    rows = []
+    for p in problems:
+        A, n = p.A, p.bcols
+        d = dev[p.name]
+        t_escs = graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream)
+        rp = torch.from_numpy(A.rowptr).to(dev["_device"])
+        ci = torch.from_numpy(A.colidx).to(dev["_device"])
+        Cs = torch.empty_like(d["C"])
+        best, best_alg = None, None
+        for alg in range(4):
+            h = bl.bl_cusparse_create(A.m, A.k, A.nnz, n, rp.data_ptr(), ci.data_ptr(),
+                                      d["vals"].data_ptr(), d["B"].data_ptr(), Cs.data_ptr(), alg, sp)
+            if not h:
+                continue
+            try:
+                t = graph_time(torch, lambda: bl.bl_cusparse_run(h, sp), stream)
+            except Exception:
+                t = None
+            bl.bl_cusparse_destroy(h)
+            if t and (best is None or t < best):
+                best, best_alg = t, alg
+        Ad = torch.from_numpy(A.dense()).to(dev["_device"])
+        Cd = torch.empty_like(d["C"])
+        t_cublas = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 0, sp), stream)
+        t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
+        del Ad
+        rows.append({"case": p.name, "escs_us": 1e3 * t_escs,
+                     "cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
+                     "cublas_us": 1e3 * t_cublas, "cublas_tf32_us": 1e3 * t_tf32,
+                     "gflops_escs": p.flops / (t_escs * 1e-3) / 1e9})
+    bl.bl_cublas_destroy(cub)
+    out = {
+        "protocol": "hot L2, CUDA graph of R calls replayed 11x, median (paper P:675 warm cache)",
+        "geomean_speedup_vs_cusparse": geomean([r["cusparse_us"] / r["escs_us"] for r in rows if r["cusparse_us"]]),
+        "geomean_speedup_vs_cublas": geomean([r["cublas_us"] / r["escs_us"] for r in rows]),
+        "geomean_speedup_vs_cublas_tf32": geomean([r["cublas_tf32_us"] / r["escs_us"] for r in rows]),
+        "pct_faster_than_cusparse": 100.0 * np.mean([r["cusparse_us"] is not None and r["escs_us"] < r["cusparse_us"] for r in rows]),
+        "pct_faster_than_cublas": 100.0 * np.mean([r["escs_us"] < r["cublas_us"] for r in rows]),
+        "cases": len(rows),
+        "paper_context": "A100: 1.84x vs cuBLAS, 2.27x vs cuSPARSE (abstract P:31); Table 1 geomeans 1.47x / 1.74x",
+    }
+    return out, rows
+
+
+def run_escs(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        pass
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    from paper_2506_15174_b200 import escs, synth
+
+    problems, desc = workload(args.workload)
+    # row-block shard of every problem; world = 1 -> whole problem
+    dev = {"_device": device}
+    shard_problems = []
+    plan_s = 0.0
+    plan_info = []
+    for p in problems:
+        r0, r1 = synth.shard_bounds(p.A.m, world, rank)
+        A = synth.row_block(p.A, r0, r1) if world > 1 else p.A
+        t0 = time.perf_counter()
+        pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols)
+        plan_s += time.perf_counter() - t0
+        info = pl.info
+        plan_info.append(info)
+        d = {"plan": pl, "A": A,
+             "vals": torch.from_numpy(A.vals).to(device) if A.nnz else torch.zeros(1, device=device),
+             "B": torch.from_numpy(p.B).to(device),
+             "C": torch.empty((A.m, p.bcols), dtype=torch.float32, device=device),
+             "flops": 2 * A.nnz * p.bcols,
+             "bytes": 8 * A.nnz + 4 * (A.m + 1) + 4 * A.k * p.bcols + 4 * A.m * p.bcols,
+             "gather_bytes": 4 * p.bcols * info["G"]}
+        dev[p.name] = d
+        shard_problems.append((p, d))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device)
+
+    def step(per_launch=None):
+        for i, (p, d) in enumerate(shard_problems):
+            if per_launch is not None:
+                per_launch[i][0].record(stream)
+            escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
+            if per_launch is not None:
+                per_launch[i][1].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    nprob = len(shard_problems)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    sleep_cycles = int(2e6 + 4e4 * nprob)
+
+    # ---- timed: step events only (value)
+    starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.zero_()
+            torch.cuda._sleep(sleep_cycles)
+            starts[s].record(stream)
+            step()
+            ends[s].record(stream)
+        barrier()
+        # ---- timed again with per-launch events (kernel durations for the roofline)
+        pl_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.zero_()
+            torch.cuda._sleep(sleep_cycles)
+            step(pl_ev[s])
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    kern_ms = np.array([[a.elapsed_time(b) for a, b in pl_ev[s]] for s in range(args.steps)])
+    kern_ms_sum = float(kern_ms.sum())
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region
+    h_vals = [torch.from_numpy(d["A"].vals).pin_memory() if d["A"].nnz else torch.zeros(1).pin_memory() for _, d in shard_problems]
+    h_B = [torch.from_numpy(p.B).pin_memory() for p, _ in shard_problems]
+    h_C = [torch.empty(d["C"].shape, dtype=torch.float32).pin_memory() for _, d in shard_problems]
+    e_vals = [torch.empty_like(d["vals"]) for _, d in shard_problems]
+    e_B = [torch.empty_like(d["B"]) for _, d in shard_problems]
+    h2d = sum(4 * d["A"].nnz + 4 * p.B.size for p, d in shard_problems)
+    d2h = sum(4 * d["C"].numel() for _, d in shard_problems)
+
+    def e2e_step():
+        for i, (p, d) in enumerate(shard_problems):
+            e_vals[i].copy_(h_vals[i], non_blocking=True)
+            e_B[i].copy_(h_B[i], non_blocking=True)
+            escs.escs_spmm(d["plan"], e_vals[i], e_B[i], d["C"], stream)
+            h_C[i].copy_(d["C"], non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    es, ee = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+    for s in range(args.steps):
+        flush.zero_()
+        torch.cuda._sleep(sleep_cycles)
+        es[s].record(stream)
+        e2e_step()
+        ee[s].record(stream)
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
+
+    # ---- reduce over ranks: flops SUM, times MAX
+    my_flops = sum(d["flops"] for _, d in shard_problems)
+    my_bytes = sum(d["bytes"] for _, d in shard_problems)
+    vec = torch.tensor([total_ms, e2e_ms, kern_ms_sum], dtype=torch.float64, device=device)
+    sums = torch.tensor([my_flops, my_bytes], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    total_ms, e2e_ms, kern_ms_sum = (float(x) for x in vec.tolist())
+    flops_all, bytes_all = (float(x) for x in sums.tolist())
+
+    result = None
+    if rank == 0:
+        hbm, peak_src, mp = peaks()
+        K = args.steps
+        value = flops_all * K / (total_ms * 1e-3) / 1e9
+        # roofline of the (only) kernel: compulsory bytes per launch / launch duration
+        achieved = my_bytes * K / (kern_ms.sum() * 1e-3) / 1e9
+        gather = sum(d["gather_bytes"] for _, d in shard_problems) * K / (kern_ms.sum() * 1e-3) / 1e9
+        per_prob = kern_ms.mean(axis=0)
+        dom = int(np.argmax(per_prob))
+        clocks = clk.summary()
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "problems": nprob, "sharding": f"row-block x{world}",
+                       "l2": "flushed before every step (256 MiB write); each problem touched once per step",
+                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "variant")}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes": "8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols per launch (CSR A, B, C once; SURVEY 8(d))",
+                         "kernel": "escs_spmm (esc_spmm_kernel), all launches of the step",
+                         "kernel_ms_per_step": float(kern_ms.sum() / K),
+                         "gather_GBps": gather,
+                         "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)"},
+            "gpu_launches": nprob * K,
+            "clocks": clocks,
+            "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "plan_seconds": plan_s,
+        }
+        if world == 1 and not args.no_cpu:
+            v, reps, secs, thr = oracle_time(problems, budget_s=args.cpu_budget)
+            result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                      "sample": f"whole workload x{reps} ({secs:.1f} s), fp64 C oracle"}
+        if world == 1 and not args.no_compare:
+            summ, rows = compare_baselines(torch, problems, dev, stream)
+            result["baselines"] = summ
+            if args.cases_out:
+                with open(args.cases_out, "w") as f:
+                    json.dump(rows, f, indent=1)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if result is not None:
+        print(json.dumps(result), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="escs", choices=["escs", "reference"])
+    ap.add_argument("--workload", default="transformer")
+    ap.add_argument("--no-compare", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=8.0)
+    ap.add_argument("--cases-out", default=None)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_escs(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,180 @@
+/*
+ * escs.h -- C ABI of the B200-native enumerate-and-sparse-coarsen (ESC) SpMM.
+ *
+ * Method: arXiv 2506.15174, "A Novel Compiler Transformation for Fast Sparse
+ * Matrix Multiplication in GPUs".  Citations: P:n = PAPER.md line n (section
+ * named), S:n = SPEC.md line n, R<k> = a reading recorded in DESIGN.md.
+ *
+ * Problem (§2 Motivation): C = A x B with A sparse M x K (CSR), B dense
+ * K x N, C dense M x N; N is "bCols" (32..128 in the paper's evaluation,
+ * P:31).  Everything is fp32 (§4.2).
+ *
+ * Life cycle (Listing 2, §3.1): the sparsity pattern of A is
+ * enumerated once on the host into a plan ("TA = dataTransformer(A, UFi, UFk)",
+ * reused across inference calls, §3.6); each product is then one
+ * kernel launch ("spmmOpt<<<...>>>").
+ *
+ * Conventions
+ *   - All functions are thread-safe; errors are reported per calling thread
+ *     through escs_last_error().
+ *   - Return codes: ESCS_OK (0) or one of the ESCS_ERR_* values below
+ *     (error convention of S:551: 1 = user error; higher = library/CUDA).
+ *   - "HOST" pointers are read only during the call; the caller keeps
+ *     ownership.  "DEVICE" pointers must be CUDA device memory on the plan's
+ *     device; the caller keeps ownership.
+ *   - Streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ *     default stream), so this header needs no CUDA include.
+ */
+#ifndef ESCS_H
+#define ESCS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    ESCS_OK = 0,
+    ESCS_ERR_ARG = 1,          /* bad argument (sizes, NULL, host-only plan)        */
+    ESCS_ERR_CSR = 2,          /* CSR violates an invariant (message names the row) */
+    ESCS_ERR_UNSUPPORTED = 3,  /* valid input outside what the kernels implement    */
+    ESCS_ERR_OOM = 4,          /* host or device allocation failed                  */
+    ESCS_ERR_CUDA = 5,         /* a CUDA runtime call failed (message has the name) */
+    ESCS_ERR_INTERNAL = 6      /* internal invariant violated (a bug)               */
+};
+
+#define ESCS_PLAN_VERSION 1
+#define ESCS_MAX_BCOLS 256     /* largest supported N (bCols)                    */
+#define ESCS_MAX_UFI 4         /* largest UFi the device kernels are built for   */
+
+typedef struct escs_plan_impl *escs_plan_t;   /* opaque, library-owned */
+
+/*
+ * escs_plan -- enumerate A's sparsity pattern (§3.2 Enumeration)
+ * and upload the plan to the current CUDA device.
+ *
+ *   m, k      rows / columns of A.  1 <= m, k < 2^31.
+ *   nnz       number of stored entries, 0 <= nnz < 2^31.
+ *   rowptr    HOST int32[m+1]: rowptr[0] = 0, non-decreasing, rowptr[m] = nnz.
+ *   colidx    HOST int32[nnz]: 0 <= colidx < k, strictly increasing per row.
+ *             Explicitly stored zeros count as structural nonzeros.
+ *   bCols     N, the number of columns of B and C: 1 <= N <= ESCS_MAX_BCOLS,
+ *             and m*N, k*N < 2^31.
+ *
+ * The plan records the panel height UFi (=h), the item size T and the kernel
+ * variant, chosen from a per-bCols parameter table (§3.5 Scheduler & Tuner,
+ * P:510-526; env override ESCS_PARAMS="ufi=4,T=64,warps=8").
+ * Synchronous, deterministic (identical inputs give byte-identical plans
+ * regardless of planner thread count).  Returns NULL on failure; the reason
+ * is in escs_last_error().  Allocates device memory with cudaMalloc on the
+ * current device; the plan is bound to that device.
+ */
+escs_plan_t escs_plan(int64_t m, int64_t k, int64_t nnz,
+                      const int32_t *rowptr, const int32_t *colidx,
+                      int32_t bCols);
+
+/*
+ * escs_spmm -- C = A x B (beta = 0: every element of C is written) with the
+ * enumerated, sparse-coarsened kernel (§3.3 Sparse Coarsen).
+ *
+ *   plan   a device plan from escs_plan / escs_plan_ex (host_only = 0).
+ *   vals   DEVICE float[nnz], A's values in CSR order (the values may change
+ *          between calls; the pattern may not).
+ *   B      DEVICE float[k * bCols], row-major (ld = bCols).
+ *   C      DEVICE float[m * bCols], row-major, overwritten.  Must not alias
+ *          vals or B.
+ *   stream cudaStream_t (as void*), may be NULL.
+ *
+ * Exactly one kernel launch, enqueue-only: no host synchronisation, no
+ * allocation, no memset -- capturable in a CUDA graph.  Two calls on the same
+ * plan must not be in flight concurrently (they share the plan's fixup
+ * workspace).  Asynchronous device faults surface at the next synchronising
+ * CUDA call, as with cuBLAS.  Pointers that are not 16-byte aligned take the
+ * scalar (generic) kernel.  Returns ESCS_OK, ESCS_ERR_ARG (NULL pointer,
+ * host-only plan, wrong device) or ESCS_ERR_CUDA (launch failure).
+ */
+int escs_spmm(escs_plan_t plan, const float *vals, const float *B, float *C,
+              void *stream);
+
+/* Release the plan's host and device memory.  NULL is a no-op.  No call on
+ * the plan may be in flight. */
+void escs_free(escs_plan_t plan);
+
+/* Code and message of the last failed call on this thread (ESCS_OK and ""
+ * if none).  The message pointer stays valid until the next ESCS call on the
+ * same thread.  msg may be NULL. */
+int escs_last_error(const char **msg);
+
+/* ------------------------------------------------------------------ *
+ * Test / tuning / benchmarking entry points                           *
+ * ------------------------------------------------------------------ */
+
+typedef struct {
+    int32_t ufi;          /* panel height h = UFi, 0 = auto; 1..16 for
+                             host-only plans, 1..ESCS_MAX_UFI for device plans   */
+    int32_t T;            /* max gcols per item (balanced tiles), 0 = auto      */
+    int32_t host_only;    /* 1: build host arrays only (no CUDA), for parity     */
+    int32_t cta_warps;    /* warps per CTA tile, 0 = auto, else 1..32            */
+    int32_t variant;      /* 0 = auto, 1 = vector (float4) kernel, 2 = scalar    */
+    int32_t ufk;          /* B-row loads in flight per sub-warp (UFk), 0 = auto  */
+    int32_t nthreads;     /* planner threads, 0 = hardware concurrency           */
+    int32_t reserved[5];  /* must be zero                                        */
+} escs_params;
+
+/* escs_plan with explicit parameters; p may be NULL (= all auto). */
+escs_plan_t escs_plan_ex(int64_t m, int64_t k, int64_t nnz,
+                         const int32_t *rowptr, const int32_t *colidx,
+                         int32_t bCols, const escs_params *p);
+
+/*
+ * The canonical plan (DESIGN.md "Canonical plan" P1-P8), host copies owned by
+ * the plan and valid until escs_free.  Array lengths: grp_* NG (+1 for the
+ * *_ptr arrays), gcol G, slot_src nnz, item_* n_items (+1 for item_gcol_ptr).
+ *   grp_panel[g], grp_mask[g]  group g = (row panel, UFi-bit pattern)
+ *   grp_col_ptr                prefix of group widths       (paper "RPP")
+ *   grp_val_ptr                prefix of popcount*width     (paper "NPP")
+ *   gcol                       group columns, ascending     (paper "Cols")
+ *   slot_src[s]                CSR position of the value at slot s (paper
+ *                              "ANNZ" order, Reading R1)
+ *   item_panel, item_group_begin, item_gcol_ptr   balanced items (Reading R7)
+ */
+typedef struct escs_plan_view {
+    int32_t header[11];   /* version, m, k, nnz, bCols, h, T, nP, NG, G, n_items */
+    const int32_t *grp_panel, *grp_mask, *grp_col_ptr, *grp_val_ptr, *gcol, *slot_src,
+                  *item_panel, *item_group_begin, *item_gcol_ptr;
+} escs_plan_view;
+
+int escs_plan_export(escs_plan_t plan, escs_plan_view *out);
+
+/* Derived, device-side facts about a plan (for tests and the bench). */
+typedef struct {
+    int32_t h, T, bcols, variant, cta_warps, ufk;
+    int32_t n_tiles;        /* CTA tiles = grid size of one escs_spmm launch     */
+    int32_t n_heavy;        /* panels split across CTA tiles (global fixup)       */
+    int32_t n_split_items;  /* items whose panel has more than one item           */
+    int32_t device;         /* CUDA ordinal, -1 for host-only plans               */
+    int64_t nP, NG, G, n_items, nnz;
+    int64_t device_bytes;   /* plan arrays + workspace resident on the device     */
+    int64_t workspace_bytes;
+    double plan_seconds;    /* host enumeration time                              */
+} escs_plan_stats;
+
+int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);
+
+/*
+ * escs_gather_probe -- measurement only (SURVEY §8(d) t_probe): the same CTA,
+ * warp and lane walk as escs_spmm with the same 128-bit B-row loads, but no
+ * values and no FMAs; writes one float per warp-lane sum into
+ * `sink` (DEVICE float[n_tiles * 32 * cta_warps]) so the loads are not dead.
+ * Its duration is the empirical gather ceiling of this plan.
+ */
+int escs_gather_probe(escs_plan_t plan, const float *B, float *sink, void *stream);
+
+/* Library version string ("escs <ver> sm_100a"). */
+const char *escs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESCS_H */

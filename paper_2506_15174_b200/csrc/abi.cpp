@@ -1,0 +1,371 @@
+// abi.cpp -- the C ABI (include/escs.h): argument checking, error reporting,
+// parameter choice, plan upload and the single launch of escs_spmm.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/escs.h"
+#include "escs_internal.h"
+
+struct escs_plan_impl {
+    escs::PlanHost host;
+    escs::Params params;
+    escs::DevPlan dev;
+    bool host_only = true;
+    int device = -1;
+    void* dmem = nullptr;
+    size_t dbytes = 0, ws_bytes = 0;
+};
+
+namespace {
+
+thread_local int g_code = ESCS_OK;
+thread_local std::string g_msg;
+
+int fail(int code, const std::string& msg) {
+    g_code = code;
+    g_msg = msg;
+    return code;
+}
+void clear_error() {
+    g_code = ESCS_OK;
+    g_msg.clear();
+}
+
+int sm_count_of_current_device() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+    return n > 0 ? n : 148;
+}
+
+// ESCS_PARAMS="ufi=4,T=64,warps=8,variant=1,ufk=4"
+void apply_env(escs::Params& p, bool& set_warps) {
+    const char* e = std::getenv("ESCS_PARAMS");
+    if (!e) return;
+    std::string s(e);
+    size_t i = 0;
+    while (i < s.size()) {
+        size_t j = s.find(',', i);
+        if (j == std::string::npos) j = s.size();
+        std::string kv = s.substr(i, j - i);
+        size_t eq = kv.find('=');
+        if (eq != std::string::npos) {
+            std::string k = kv.substr(0, eq);
+            int v = std::atoi(kv.c_str() + eq + 1);
+            if (k == "ufi") p.h = v;
+            else if (k == "T") p.T = v;
+            else if (k == "warps") { p.cta_warps = v; set_warps = true; }
+            else if (k == "variant") p.variant = v;
+            else if (k == "ufk") p.ufk = v;
+        }
+        i = j + 1;
+    }
+}
+
+// Warps per CTA tile: a multiple of the typical number of items per panel, so
+// that whole panels fill tiles without idle warps (about 8 warps per CTA).
+int auto_cta_warps(const escs::PlanHost& ph) {
+    const int64_t nP = ph.header[7];
+    const int64_t NI = ph.item_panel.size();
+    if (nP == 0) return 8;
+    std::vector<int32_t> per(nP, 0);
+    for (int64_t i = 0; i < NI; i++) per[ph.item_panel[i]]++;
+    std::nth_element(per.begin(), per.begin() + nP / 2, per.end());
+    const int typ = std::max(1, per[nP / 2]);
+    if (typ >= 16) return 16;
+    return std::max(1, typ * std::max(1, 8 / typ));
+}
+
+template <class T>
+size_t add_region(size_t& off, size_t count) {
+    off = (off + 255) & ~size_t(255);
+    size_t at = off;
+    off += count * sizeof(T);
+    return at;
+}
+
+#define CUDA_TRY(call)                                                                 \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            fail(ESCS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+            return false;                                                              \
+        }                                                                              \
+    } while (0)
+
+bool upload(escs_plan_impl* P) {
+    auto& ph = P->host;
+    auto& dp = P->dev;
+    const int h = ph.header[5], n = ph.header[4];
+    const int64_t NG = ph.header[8], G = ph.header[9], NI = ph.header[10], nnz = ph.header[3];
+    // device group records: col_begin, col_end, val_begin, mask
+    std::vector<int32_t> grp(4 * NG), items(4 * NI);
+    for (int64_t g = 0; g < NG; g++) {
+        grp[4 * g + 0] = ph.grp_col_ptr[g];
+        grp[4 * g + 1] = ph.grp_col_ptr[g + 1];
+        grp[4 * g + 2] = ph.grp_val_ptr[g];
+        grp[4 * g + 3] = ph.grp_mask[g];
+    }
+    for (int64_t i = 0; i < NI; i++) {
+        items[4 * i + 0] = ph.item_panel[i];
+        items[4 * i + 1] = ph.item_group_begin[i];
+        items[4 * i + 2] = ph.item_gcol_ptr[i];
+        items[4 * i + 3] = ph.item_gcol_ptr[i + 1];
+    }
+    size_t off = 0;
+    const size_t o_grp = add_region<int32_t>(off, 4 * NG);
+    const size_t o_gcol = add_region<int32_t>(off, G);
+    const size_t o_slot = add_region<int32_t>(off, nnz);
+    const size_t o_items = add_region<int32_t>(off, 4 * NI);
+    const size_t o_aux = add_region<int32_t>(off, NI);
+    const size_t o_tiles = add_region<int32_t>(off, ph.tile_info.size());
+    const size_t o_heavy = add_region<int32_t>(off, ph.heavy_info.size());
+    const size_t o_cnt = add_region<int32_t>(off, ph.n_heavy);
+    const size_t ws_elems = (size_t)ph.n_heavy_tiles * h * n;
+    const size_t o_ws = add_region<float>(off, ws_elems);
+    off = std::max<size_t>(off, 256);
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, off);
+    if (e != cudaSuccess) {
+        fail(e == cudaErrorMemoryAllocation ? ESCS_ERR_OOM : ESCS_ERR_CUDA,
+             std::string("cudaMalloc(") + std::to_string(off) + "): " + cudaGetErrorString(e));
+        return false;
+    }
+    P->dmem = d;
+    P->dbytes = off;
+    P->ws_bytes = ws_elems * sizeof(float);
+    char* b = static_cast<char*>(d);
+    auto put = [&](size_t o, const void* src, size_t bytes) -> bool {
+        if (!bytes) return true;
+        CUDA_TRY(cudaMemcpy(b + o, src, bytes, cudaMemcpyHostToDevice));
+        return true;
+    };
+    if (!put(o_grp, grp.data(), grp.size() * 4)) return false;
+    if (!put(o_gcol, ph.gcol.data(), G * 4)) return false;
+    if (!put(o_slot, ph.slot_src.data(), nnz * 4)) return false;
+    if (!put(o_items, items.data(), items.size() * 4)) return false;
+    if (!put(o_aux, ph.item_aux.data(), NI * 4)) return false;
+    if (!put(o_tiles, ph.tile_info.data(), ph.tile_info.size() * 4)) return false;
+    if (!put(o_heavy, ph.heavy_info.data(), ph.heavy_info.size() * 4)) return false;
+    if (ph.n_heavy) CUDA_TRY(cudaMemset(b + o_cnt, 0, ph.n_heavy * 4));
+    dp.grp = reinterpret_cast<const int32_t*>(b + o_grp);
+    dp.gcol = reinterpret_cast<const int32_t*>(b + o_gcol);
+    dp.slot = reinterpret_cast<const int32_t*>(b + o_slot);
+    dp.items = reinterpret_cast<const int32_t*>(b + o_items);
+    dp.item_aux = reinterpret_cast<const int32_t*>(b + o_aux);
+    dp.tiles = reinterpret_cast<const int32_t*>(b + o_tiles);
+    dp.heavy = reinterpret_cast<const int32_t*>(b + o_heavy);
+    dp.counters = reinterpret_cast<int32_t*>(b + o_cnt);
+    dp.ws = reinterpret_cast<float*>(b + o_ws);
+    CUDA_TRY(cudaDeviceSynchronize());
+    return true;
+}
+
+escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, int32_t bCols, const escs_params* ep) {
+    clear_error();
+    if (m < 1 || k < 1 || nnz < 0 || bCols < 1) {
+        fail(ESCS_ERR_ARG, "m, k, bCols must be >= 1 and nnz >= 0");
+        return nullptr;
+    }
+    const int64_t lim = (int64_t)1 << 31;
+    if (m >= lim || k >= lim || nnz >= lim || m * bCols >= lim || k * bCols >= lim) {
+        fail(ESCS_ERR_ARG, "m, k, nnz, m*bCols and k*bCols must be < 2^31");
+        return nullptr;
+    }
+    if (bCols > ESCS_MAX_BCOLS) {
+        fail(ESCS_ERR_UNSUPPORTED, "bCols > ESCS_MAX_BCOLS (256)");
+        return nullptr;
+    }
+    if (ep) {
+        for (int i = 0; i < 5; i++)
+            if (ep->reserved[i] != 0) {
+                fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
+                return nullptr;
+            }
+    }
+    std::string v = escs::validate_csr(m, k, nnz, rowptr, colidx);
+    if (!v.empty()) {
+        fail(ESCS_ERR_CSR, "invalid CSR: " + v);
+        return nullptr;
+    }
+    const bool host_only = ep && ep->host_only;
+    int device = -1;
+    if (!host_only) {
+        cudaError_t e = cudaGetDevice(&device);
+        if (e != cudaSuccess) {
+            fail(ESCS_ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+            return nullptr;
+        }
+    }
+    escs::Params p = escs::choose_params(m, k, nnz, bCols, host_only ? 148 : sm_count_of_current_device());
+    bool set_warps = false;
+    apply_env(p, set_warps);
+    if (ep) {
+        if (ep->ufi) p.h = ep->ufi;
+        if (ep->T) p.T = ep->T;
+        if (ep->cta_warps) { p.cta_warps = ep->cta_warps; set_warps = true; }
+        if (ep->variant) p.variant = ep->variant;
+        if (ep->ufk) p.ufk = ep->ufk;
+        if (ep->nthreads) p.nthreads = ep->nthreads;
+    }
+    if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > 16)) ||
+        p.variant < 1 || p.variant > 2) {
+        fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16, variant 1..2)");
+        return nullptr;
+    }
+    if (p.variant == 1 && !(bCols == 32 || bCols == 64 || bCols == 128 || bCols == 256)) p.variant = 2;
+    if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk)) {
+        fail(ESCS_ERR_UNSUPPORTED, "no kernel for ufi=" + std::to_string(p.h) + " bCols=" +
+                                       std::to_string(bCols) + " variant=" +
+                                       std::to_string(p.variant) + " ufk=" + std::to_string(p.ufk));
+        return nullptr;
+    }
+    escs_plan_impl* P = new (std::nothrow) escs_plan_impl();
+    if (!P) {
+        fail(ESCS_ERR_OOM, "host allocation");
+        return nullptr;
+    }
+    try {
+        escs::build_plan(m, k, nnz, rowptr, colidx, bCols, p, P->host);
+        if (!set_warps) p.cta_warps = auto_cta_warps(P->host);
+        escs::build_tiles(P->host, p.cta_warps);
+    } catch (const std::bad_alloc&) {
+        delete P;
+        fail(ESCS_ERR_OOM, "host allocation while planning");
+        return nullptr;
+    } catch (const std::exception& ex) {
+        delete P;
+        fail(ESCS_ERR_INTERNAL, ex.what());
+        return nullptr;
+    }
+    P->params = p;
+    P->host_only = host_only;
+    P->device = device;
+    auto& dp = P->dev;
+    dp.m = (int)m; dp.k = (int)k; dp.bcols = bCols; dp.h = p.h;
+    dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
+    dp.ufk = p.ufk; dp.any_sync = P->host.any_sync;
+    if (!host_only) {
+        if (!upload(P)) {
+            escs_free(P);
+            return nullptr;
+        }
+        int e = escs::prepare_kernels(dp);
+        if (e) {
+            fail(ESCS_ERR_CUDA, std::string("kernel attributes: ") +
+                                    cudaGetErrorString((cudaError_t)e));
+            escs_free(P);
+            return nullptr;
+        }
+    }
+    return P;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+escs_plan_t escs_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, int32_t bCols) {
+    return make_plan(m, k, nnz, rowptr, colidx, bCols, nullptr);
+}
+
+escs_plan_t escs_plan_ex(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                         const int32_t* colidx, int32_t bCols, const escs_params* p) {
+    return make_plan(m, k, nnz, rowptr, colidx, bCols, p);
+}
+
+int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, void* stream) {
+    clear_error();
+    if (!plan) return fail(ESCS_ERR_ARG, "plan is NULL");
+    if (plan->host_only) return fail(ESCS_ERR_ARG, "plan is host-only (escs_params.host_only=1)");
+    if (!B || !C || (!vals && plan->host.header[3] > 0))
+        return fail(ESCS_ERR_ARG, "vals, B and C must be non-NULL device pointers");
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev != plan->device)
+        return fail(ESCS_ERR_ARG, "current device " + std::to_string(dev) +
+                                      " differs from the plan's device " +
+                                      std::to_string(plan->device));
+    const bool vec_ok = aligned16(B) && aligned16(C);
+    int e = escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok);
+    if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
+                                          cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
+int escs_gather_probe(escs_plan_t plan, const float* B, float* sink, void* stream) {
+    clear_error();
+    if (!plan || plan->host_only || !B || !sink) return fail(ESCS_ERR_ARG, "bad probe arguments");
+    const bool vec_ok = aligned16(B);
+    int e = escs::launch_probe(plan->dev, B, sink, stream, vec_ok);
+    if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") +
+                                                 cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
+void escs_free(escs_plan_t plan) {
+    if (!plan) return;
+    if (plan->dmem) cudaFree(plan->dmem);
+    delete plan;
+}
+
+int escs_last_error(const char** msg) {
+    if (msg) *msg = g_msg.c_str();
+    return g_code;
+}
+
+int escs_plan_export(escs_plan_t plan, escs_plan_view* out) {
+    clear_error();
+    if (!plan || !out) return fail(ESCS_ERR_ARG, "NULL argument");
+    const auto& h = plan->host;
+    std::memcpy(out->header, h.header, sizeof(out->header));
+    out->grp_panel = h.grp_panel.data();
+    out->grp_mask = h.grp_mask.data();
+    out->grp_col_ptr = h.grp_col_ptr.data();
+    out->grp_val_ptr = h.grp_val_ptr.data();
+    out->gcol = h.gcol.data();
+    out->slot_src = h.slot_src.data();
+    out->item_panel = h.item_panel.data();
+    out->item_group_begin = h.item_group_begin.data();
+    out->item_gcol_ptr = h.item_gcol_ptr.data();
+    return ESCS_OK;
+}
+
+int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
+    clear_error();
+    if (!plan || !o) return fail(ESCS_ERR_ARG, "NULL argument");
+    const auto& h = plan->host;
+    std::memset(o, 0, sizeof(*o));
+    o->h = plan->params.h;
+    o->T = plan->params.T;
+    o->bcols = h.header[4];
+    o->variant = plan->params.variant;
+    o->cta_warps = plan->params.cta_warps;
+    o->ufk = plan->params.ufk;
+    o->n_tiles = h.n_tiles;
+    o->n_heavy = h.n_heavy;
+    o->n_split_items = h.n_split_items;
+    o->device = plan->device;
+    o->nP = h.header[7];
+    o->NG = h.header[8];
+    o->G = h.header[9];
+    o->n_items = h.header[10];
+    o->nnz = h.header[3];
+    o->device_bytes = (int64_t)plan->dbytes;
+    o->workspace_bytes = (int64_t)plan->ws_bytes;
+    o->plan_seconds = h.plan_seconds;
+    return ESCS_OK;
+}
+
+const char* escs_version(void) { return "escs 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// escs_internal.h -- shared between the host planner/ABI (C++) and the
+// sm_100a kernels (CUDA).  Not part of the public ABI (include/escs.h).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace escs {
+
+// Parameters recorded in the plan (§3.5 Scheduler & Tuner).
+struct Params {
+    int h = 4;          // UFi: rows per panel
+    int T = 64;         // max gcols per item
+    int cta_warps = 8;  // warps per CTA tile
+    int variant = 1;    // 1 = vector (float4) lane map, 2 = scalar lane map
+    int ufk = 4;        // B-row loads in flight per sub-warp step (UFk)
+    int nthreads = 0;   // planner threads
+};
+
+// Host plan: the canonical arrays (P1-P8) plus the device-only
+// derived CTA-tile schedule.
+struct PlanHost {
+    int32_t header[11] = {0};
+    std::vector<int32_t> grp_panel, grp_mask, grp_col_ptr, grp_val_ptr, gcol, slot_src;
+    std::vector<int32_t> item_panel, item_group_begin, item_gcol_ptr;
+    // derived (not part of plan parity; deterministic)
+    std::vector<int32_t> item_aux;    // lead | cnt << 8  (warp slot of the panel's first
+                                      // item inside the tile, #items of the panel there)
+    std::vector<int32_t> tile_info;   // 4 per tile: item_begin, item_end, heavy_id, flags
+                                      // flags: bit0 needs_sync, bits 1.. = ordinal q
+    std::vector<int32_t> heavy_info;  // 4 per heavy panel: panel, ws_base, ntiles, 0
+    int n_tiles = 0, n_heavy = 0, n_heavy_tiles = 0, n_split_items = 0;
+    bool any_sync = false;
+    double plan_seconds = 0.0;
+};
+
+// Validate the CSR.  Returns "" when valid, else a message.
+std::string validate_csr(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                         const int32_t* colidx);
+
+// Build the canonical plan + tiles.  Throws std::runtime_error on bad params.
+void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                const int32_t* colidx, int32_t bcols, const Params& p, PlanHost& out);
+
+// Auto parameters from the per-bCols table and the problem size.
+Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm);
+
+// Pick cta_warps from the item distribution and build the tile schedule.
+void build_tiles(PlanHost& ph, int cta_warps);
+
+// Device-side view used by the kernels.
+struct DevPlan {
+    const int32_t* grp = nullptr;       // int4[NG]: col_begin, col_end, val_begin, mask
+    const int32_t* gcol = nullptr;      // int32[G]
+    const int32_t* slot = nullptr;      // int32[nnz]
+    const int32_t* items = nullptr;     // int4[n_items]: panel, group_begin, gcol_begin, gcol_end
+    const int32_t* item_aux = nullptr;  // int32[n_items]
+    const int32_t* tiles = nullptr;     // int4[n_tiles]
+    const int32_t* heavy = nullptr;     // int4[n_heavy]
+    float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
+    int32_t* counters = nullptr;        // int32[n_heavy]
+    int m = 0, k = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4;
+    bool any_sync = false;
+};
+
+// Launch the ESC SpMM kernel (one launch).  Returns a cudaError_t value.
+int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
+                bool vec_ok);
+// Launch the gather probe (same walk, loads only).
+int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok);
+// Prepare kernel attributes (dynamic smem limits) once per plan.
+int prepare_kernels(const DevPlan& dp);
+// Does a kernel instance exist for this configuration?
+bool kernel_supported(int h, int bcols, int variant, int ufk);
+size_t smem_bytes(const DevPlan& dp);
+
+}  // namespace escs

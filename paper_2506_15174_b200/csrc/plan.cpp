@@ -1,0 +1,315 @@
+// plan.cpp -- host enumeration planner (§3.2 Enumeration) and the
+// data transformation of §3.3.3, built from CSR in O(nnz * UFi)
+// by an UFi-way merge of each panel's sorted rows.  The paper's own
+// dataTransformer scans dense A in O(M*K); that form is the
+// oracle's (oracle/escs_oracle.c) and shares no code with this file.  The two
+// must agree byte for byte (tests/test_plan_parity.py).
+//
+// Canonical plan (P1-P8):
+//   panel P = rows [P*h, min(m,(P+1)*h))                      (R2)
+//   gcol    = (panel, column) with >= 1 nonzero, pattern = UFi-bit row mask
+//   groups  = (panel, mask) ordered by panel then mask ascending   (R3, Fig. 4)
+//   slots   = column-major over a group's columns, pattern rows ascending
+//             (Listing 7's t_nnz cursor, Reading R1)
+//   items   = panel stream cut into n_P = max(1, ceil(S_P/T)) even pieces (R7)
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+
+#include "escs_internal.h"
+
+namespace escs {
+
+std::string validate_csr(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                         const int32_t* colidx) {
+    if (!rowptr) return "rowptr is NULL";
+    if (nnz > 0 && !colidx) return "colidx is NULL";
+    if (rowptr[0] != 0) return "rowptr[0] != 0";
+    if ((int64_t)rowptr[m] != nnz) return "rowptr[m] != nnz";
+    for (int64_t i = 0; i < m; i++) {
+        int64_t a = rowptr[i], b = rowptr[i + 1];
+        if (b < a) return "rowptr decreases at row " + std::to_string(i);
+        if (b > nnz) return "rowptr exceeds nnz at row " + std::to_string(i);
+        for (int64_t t = a; t < b; t++) {
+            int32_t c = colidx[t];
+            if (c < 0 || c >= k)
+                return "column index out of range at row " + std::to_string(i) + " position " +
+                       std::to_string(t);
+            if (t > a && c <= colidx[t - 1])
+                return "column indices not strictly increasing at row " + std::to_string(i) +
+                       " position " + std::to_string(t);
+        }
+    }
+    return "";
+}
+
+namespace {
+
+// One chunk of consecutive panels, planned independently then concatenated.
+struct Chunk {
+    int64_t p0 = 0, p1 = 0;
+    std::vector<int32_t> grp_panel, grp_mask, grp_w, grp_vw;   // widths, value widths
+    std::vector<int32_t> gcol, slot;
+    std::vector<int32_t> item_panel, item_gb_local, item_s1_local;
+};
+
+void plan_chunk(const int32_t* rowptr, const int32_t* colidx, int64_t m, int h, int T,
+                Chunk& ch) {
+    const int nmask = 1 << h;
+    std::vector<int32_t> cur(h), end(h);
+    std::vector<int32_t> e_col, e_mask, e_pos;   // merged entries and their CSR positions
+    std::vector<int32_t> e_off;
+    std::vector<int64_t> cnt(nmask), gstart(nmask), vstart(nmask), gslot(nmask);
+    std::vector<int32_t> gidx(nmask);
+
+    for (int64_t P = ch.p0; P < ch.p1; P++) {
+        const int64_t r0 = P * h;
+        const int rows = (int)std::min<int64_t>(h, m - r0);
+        for (int r = 0; r < h; r++) {
+            if (r < rows) {
+                cur[r] = rowptr[r0 + r];
+                end[r] = rowptr[r0 + r + 1];
+            } else {
+                cur[r] = end[r] = 0;
+            }
+        }
+        e_col.clear(); e_mask.clear(); e_pos.clear(); e_off.clear();
+        // UFi-way merge: smallest pending column across the panel's rows.
+        for (;;) {
+            int32_t c = INT32_MAX;
+            for (int r = 0; r < rows; r++)
+                if (cur[r] < end[r] && colidx[cur[r]] < c) c = colidx[cur[r]];
+            if (c == INT32_MAX) break;
+            int32_t mask = 0;
+            e_off.push_back((int32_t)e_pos.size());
+            for (int r = 0; r < rows; r++)
+                if (cur[r] < end[r] && colidx[cur[r]] == c) {
+                    mask |= 1 << r;
+                    e_pos.push_back(cur[r]++);   // ranks ascend with r
+                }
+            e_col.push_back(c);
+            e_mask.push_back(mask);
+        }
+        const int64_t ne = (int64_t)e_col.size();
+        // stable counting sort of entries by mask -> groups
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t e = 0; e < ne; e++) cnt[e_mask[e]]++;
+        const int64_t g_first = (int64_t)ch.grp_panel.size();
+        const int64_t col_base = (int64_t)ch.gcol.size();
+        const int64_t val_base = (int64_t)ch.slot.size();
+        int64_t s = 0, v = 0;
+        for (int mu = 1; mu < nmask; mu++) {
+            if (!cnt[mu]) continue;
+            const int p = __builtin_popcount((unsigned)mu);
+            gidx[mu] = (int32_t)ch.grp_panel.size();
+            gstart[mu] = s;
+            vstart[mu] = v;
+            gslot[mu] = 0;
+            ch.grp_panel.push_back((int32_t)P);
+            ch.grp_mask.push_back(mu);
+            ch.grp_w.push_back((int32_t)cnt[mu]);
+            ch.grp_vw.push_back((int32_t)(cnt[mu] * p));
+            s += cnt[mu];
+            v += cnt[mu] * p;
+        }
+        ch.gcol.resize(col_base + s);
+        ch.slot.resize(val_base + v);
+        for (int64_t e = 0; e < ne; e++) {
+            const int mu = e_mask[e];
+            const int p = __builtin_popcount((unsigned)mu);
+            const int64_t ci = gslot[mu]++;
+            ch.gcol[col_base + gstart[mu] + ci] = e_col[e];
+            int32_t* dst = &ch.slot[val_base + vstart[mu] + ci * p];
+            for (int j = 0; j < p; j++) dst[j] = e_pos[e_off[e] + j];
+        }
+        // balanced items over the panel stream of length s
+        const int64_t SP = s;
+        int64_t n = (SP + T - 1) / T;
+        if (n < 1) n = 1;
+        const int64_t ng = (int64_t)ch.grp_panel.size() - g_first;
+        int64_t gb = 0;   // monotone pointer: last group with stream start <= s0
+        for (int64_t q = 0; q < n; q++) {
+            const int64_t s0 = (q * SP) / n, s1 = ((q + 1) * SP) / n;
+            while (gb + 1 < ng && gstart[ch.grp_mask[g_first + gb + 1]] <= s0) gb++;
+            ch.item_panel.push_back((int32_t)P);
+            ch.item_gb_local.push_back((int32_t)(g_first + gb));
+            ch.item_s1_local.push_back((int32_t)(col_base + s1));
+        }
+    }
+}
+
+}  // namespace
+
+void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
+                int32_t bcols, const Params& p, PlanHost& out) {
+    auto t0 = std::chrono::steady_clock::now();
+    const int h = p.h, T = p.T;
+    if (h < 1 || h > 16) throw std::runtime_error("ufi must be in 1..16");
+    if (T < 1) throw std::runtime_error("T must be >= 1");
+    const int64_t nP = (m + h - 1) / h;
+
+    // chunks of consecutive panels balanced by nnz
+    int nth = p.nthreads > 0 ? p.nthreads : (int)std::max(1u, std::thread::hardware_concurrency());
+    if (nnz < 200000) nth = 1;
+    const int64_t nchunks = std::min<int64_t>(nP, (int64_t)nth * 8);
+    std::vector<Chunk> chunks(nchunks);
+    {
+        int64_t P = 0;
+        for (int64_t c = 0; c < nchunks; c++) {
+            const int64_t target = (nnz * (c + 1)) / nchunks;
+            int64_t P1 = P + 1;
+            if (c == nchunks - 1) {
+                P1 = nP;
+            } else {
+                // advance until the chunk's cumulative nnz reaches target, leaving
+                // at least one panel for each remaining chunk
+                while (P1 < nP - (nchunks - 1 - c) &&
+                       rowptr[std::min<int64_t>(m, P1 * h)] < target)
+                    P1++;
+            }
+            chunks[c].p0 = P;
+            chunks[c].p1 = P1;
+            P = P1;
+        }
+    }
+    if (nth <= 1 || nchunks <= 1) {
+        for (auto& ch : chunks) plan_chunk(rowptr, colidx, m, h, T, ch);
+    } else {
+        std::vector<std::thread> th;
+        std::atomic<int64_t> next{0};
+        for (int t = 0; t < nth; t++)
+            th.emplace_back([&] {
+                for (;;) {
+                    int64_t c = next.fetch_add(1);
+                    if (c >= nchunks) break;
+                    plan_chunk(rowptr, colidx, m, h, T, chunks[c]);
+                }
+            });
+        for (auto& x : th) x.join();
+    }
+
+    // deterministic concatenation in panel order
+    int64_t NG = 0, G = 0, V = 0, NI = 0;
+    for (auto& ch : chunks) {
+        NG += ch.grp_panel.size();
+        G += ch.gcol.size();
+        V += ch.slot.size();
+        NI += ch.item_panel.size();
+    }
+    if (V != nnz) throw std::runtime_error("internal: slot count != nnz");
+    if (NG >= INT32_MAX || G >= INT32_MAX || NI >= INT32_MAX)
+        throw std::runtime_error("plan too large for int32 indices");
+    out.grp_panel.resize(NG); out.grp_mask.resize(NG);
+    out.grp_col_ptr.resize(NG + 1); out.grp_val_ptr.resize(NG + 1);
+    out.gcol.resize(G); out.slot_src.resize(nnz);
+    out.item_panel.resize(NI); out.item_group_begin.resize(NI); out.item_gcol_ptr.resize(NI + 1);
+    out.grp_col_ptr[0] = 0; out.grp_val_ptr[0] = 0; out.item_gcol_ptr[0] = 0;
+    int64_t og = 0, oc = 0, ov = 0, oi = 0;
+    for (auto& ch : chunks) {
+        const int64_t ng = ch.grp_panel.size();
+        for (int64_t g = 0; g < ng; g++) {
+            out.grp_panel[og + g] = ch.grp_panel[g];
+            out.grp_mask[og + g] = ch.grp_mask[g];
+            out.grp_col_ptr[og + g + 1] = out.grp_col_ptr[og + g] + ch.grp_w[g];
+            out.grp_val_ptr[og + g + 1] = out.grp_val_ptr[og + g] + ch.grp_vw[g];
+        }
+        if (!ch.gcol.empty()) std::memcpy(&out.gcol[oc], ch.gcol.data(), ch.gcol.size() * 4);
+        if (!ch.slot.empty()) std::memcpy(&out.slot_src[ov], ch.slot.data(), ch.slot.size() * 4);
+        const int64_t ni = ch.item_panel.size();
+        for (int64_t i = 0; i < ni; i++) {
+            out.item_panel[oi + i] = ch.item_panel[i];
+            out.item_group_begin[oi + i] = (int32_t)(og + ch.item_gb_local[i]);
+            out.item_gcol_ptr[oi + i + 1] = (int32_t)(oc + ch.item_s1_local[i]);
+        }
+        og += ng; oc += ch.gcol.size(); ov += ch.slot.size(); oi += ni;
+    }
+    int32_t* hd = out.header;
+    hd[0] = 1; hd[1] = (int32_t)m; hd[2] = (int32_t)k; hd[3] = (int32_t)nnz; hd[4] = bcols;
+    hd[5] = h; hd[6] = T; hd[7] = (int32_t)nP; hd[8] = (int32_t)NG; hd[9] = (int32_t)G;
+    hd[10] = (int32_t)NI;
+    out.plan_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// CTA tiles: whole panels are packed greedily (in panel order) into tiles of
+// at most W items, so that a panel split into several items is combined in
+// shared memory by one CTA.  A panel with more than W items ("heavy", the
+// power-law case C4) gets ceil(n/W) exclusive tiles that are combined through
+// a global workspace in tile order (deterministic fixup).
+void build_tiles(PlanHost& ph, int W) {
+    const int64_t NI = ph.item_panel.size();
+    const int64_t nP = ph.header[7];
+    ph.item_aux.assign(NI, 0);
+    ph.tile_info.clear();
+    ph.heavy_info.clear();
+    ph.n_heavy = ph.n_heavy_tiles = ph.n_split_items = 0;
+    ph.any_sync = false;
+    int64_t cur_begin = 0, cur_end = 0;
+    bool cur_sync = false;
+    auto close = [&]() {
+        if (cur_end > cur_begin) {
+            ph.tile_info.insert(ph.tile_info.end(),
+                                {(int32_t)cur_begin, (int32_t)cur_end, -1, cur_sync ? 1 : 0});
+            ph.any_sync |= cur_sync;
+        }
+        cur_begin = cur_end;
+        cur_sync = false;
+    };
+    int64_t i = 0;
+    for (int64_t P = 0; P < nP; P++) {
+        int64_t a = i;
+        while (i < NI && ph.item_panel[i] == P) i++;
+        const int64_t n = i - a;
+        if (n > 1) ph.n_split_items += (int32_t)n;
+        if (n > W) {
+            close();
+            const int64_t nt = (n + W - 1) / W;
+            const int hid = ph.n_heavy++;
+            ph.heavy_info.insert(ph.heavy_info.end(),
+                                 {(int32_t)P, ph.n_heavy_tiles, (int32_t)nt, 0});
+            for (int64_t q = 0; q < nt; q++) {
+                const int64_t b0 = a + (q * n) / nt, b1 = a + ((q + 1) * n) / nt;
+                for (int64_t j = b0; j < b1; j++)
+                    ph.item_aux[j] = 0 | ((int32_t)(b1 - b0) << 8);
+                ph.tile_info.insert(ph.tile_info.end(),
+                                    {(int32_t)b0, (int32_t)b1, hid, (int32_t)(1 | (q << 1))});
+            }
+            ph.n_heavy_tiles += (int32_t)nt;
+            ph.any_sync = true;
+            cur_begin = cur_end = i;
+            continue;
+        }
+        if (cur_end - cur_begin + n > W) close();
+        const int32_t lead = (int32_t)(a - cur_begin);
+        for (int64_t j = a; j < i; j++) ph.item_aux[j] = lead | ((int32_t)n << 8);
+        if (n > 1) cur_sync = true;
+        cur_end = i;
+    }
+    close();
+    ph.n_tiles = (int)(ph.tile_info.size() / 4);
+}
+
+Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
+    Params p;
+    p.h = 4;
+    p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
+    p.ufk = 4;
+    // expected gcols for a uniform pattern at h=4; item size so
+    // that about 64 warps per SM are available, clamped.
+    const double d = (double)nnz / ((double)m * (double)k);
+    const double s = 1.0 - d;
+    const double G = std::ceil((double)m / p.h) * (double)k * (1.0 - std::pow(s, p.h));
+    const double target_items = (double)n_sm * 64.0;
+    int64_t T = (int64_t)std::ceil(G / target_items);
+    T = std::max<int64_t>(T, 16);
+    T = std::min<int64_t>(T, 1 << 20);
+    p.T = (int)T;
+    p.cta_warps = 0;   // auto from the item distribution
+    return p;
+}
+
+}  // namespace escs

@@ -1,0 +1,223 @@
+"""Thin ctypes binding over libescs.so (include/escs.h) -- marshalling only.
+
+Every step of the hot path runs inside the library: the host planner and the
+sm_100a kernel.  There is no Python or CPU fallback: if ``libescs.so`` is
+missing this module raises at import time.  torch is used only to hand over
+device pointers and the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libescs.so")
+
+ESCS_OK, ESCS_ERR_ARG, ESCS_ERR_CSR, ESCS_ERR_UNSUPPORTED, ESCS_ERR_OOM, ESCS_ERR_CUDA, \
+    ESCS_ERR_INTERNAL = range(7)
+HEADER_FIELDS = ("version", "m", "k", "nnz", "bCols", "h", "T", "nP", "NG", "G", "n_items")
+PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "slot_src",
+               "item_panel", "item_group_begin", "item_gcol_ptr")
+EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
+                    "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
+                      "`python -m paper_2506_15174_b200.build` (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("ufi", ctypes.c_int32), ("T", ctypes.c_int32), ("host_only", ctypes.c_int32),
+                ("cta_warps", ctypes.c_int32), ("variant", ctypes.c_int32), ("ufk", ctypes.c_int32),
+                ("nthreads", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+class _View(ctypes.Structure):
+    _fields_ = [("header", ctypes.c_int32 * 11)] + \
+               [(n, ctypes.POINTER(ctypes.c_int32)) for n in PLAN_ARRAYS]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("h", "T", "bcols", "variant", "cta_warps", "ufk",
+                                              "n_tiles", "n_heavy", "n_split_items", "device")] + \
+               [(n, ctypes.c_int64) for n in ("nP", "NG", "G", "n_items", "nnz", "device_bytes",
+                                              "workspace_bytes")] + \
+               [("plan_seconds", ctypes.c_double)]
+
+
+_vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+_lib.escs_plan.argtypes = [_i64, _i64, _i64, _vp, _vp, _i32]
+_lib.escs_plan.restype = _vp
+_lib.escs_plan_ex.argtypes = [_i64, _i64, _i64, _vp, _vp, _i32, ctypes.POINTER(_Params)]
+_lib.escs_plan_ex.restype = _vp
+_lib.escs_spmm.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.escs_spmm.restype = ctypes.c_int
+_lib.escs_gather_probe.argtypes = [_vp, _vp, _vp, _vp]
+_lib.escs_gather_probe.restype = ctypes.c_int
+_lib.escs_free.argtypes = [_vp]
+_lib.escs_free.restype = None
+_lib.escs_last_error.argtypes = [ctypes.POINTER(ctypes.c_char_p)]
+_lib.escs_last_error.restype = ctypes.c_int
+_lib.escs_plan_export.argtypes = [_vp, ctypes.POINTER(_View)]
+_lib.escs_plan_export.restype = ctypes.c_int
+_lib.escs_plan_info.argtypes = [_vp, ctypes.POINTER(_Stats)]
+_lib.escs_plan_info.restype = ctypes.c_int
+_lib.escs_version.argtypes = []
+_lib.escs_version.restype = ctypes.c_char_p
+
+
+class EscsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"escs error {code}: {msg}")
+        self.code = code
+
+
+def escs_last_error():
+    msg = ctypes.c_char_p()
+    code = _lib.escs_last_error(ctypes.byref(msg))
+    return code, (msg.value or b"").decode()
+
+
+def _raise_last():
+    code, msg = escs_last_error()
+    raise EscsError(code, msg)
+
+
+def escs_version() -> str:
+    return _lib.escs_version().decode()
+
+
+class Plan:
+    """Owns an escs_plan_t; freed on close() / garbage collection."""
+
+    def __init__(self, handle, m, k, nnz, bcols):
+        self.handle = handle
+        self.m, self.k, self.nnz, self.bcols = m, k, nnz, bcols
+
+    def close(self):
+        if self.handle:
+            _lib.escs_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def info(self):
+        return escs_plan_info(self)
+
+    def export(self):
+        return escs_plan_export(self)
+
+
+def _csr_args(rowptr, colidx):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int32)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    return rowptr, colidx
+
+
+def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
+    """Enumerate A's pattern and upload the plan (host int32 CSR arrays)."""
+    rowptr, colidx = _csr_args(rowptr, colidx)
+    h = _lib.escs_plan(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
+                       int(bCols))
+    if not h:
+        _raise_last()
+    return Plan(h, int(m), int(k), int(nnz), int(bCols))
+
+
+def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
+                 variant=0, ufk=0, nthreads=0) -> Plan:
+    rowptr, colidx = _csr_args(rowptr, colidx)
+    p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
+                int(nthreads), (ctypes.c_int32 * 5)())
+    h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
+                          int(bCols), ctypes.byref(p))
+    if not h:
+        _raise_last()
+    return Plan(h, int(m), int(k), int(nnz), int(bCols))
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def escs_spmm(plan: Plan, vals, B, C, stream=None) -> None:
+    """C = A x B on `stream` (default: torch's current stream).  vals/B/C are
+    device torch tensors (fp32, contiguous) or raw device pointers (int)."""
+    for t in (vals, B, C):
+        if t is not None and not isinstance(t, int):
+            if not t.is_cuda or t.dtype.itemsize != 4 or not t.is_contiguous():
+                raise EscsError(ESCS_ERR_ARG, "vals, B, C must be contiguous fp32 CUDA tensors")
+    if not isinstance(B, int) and B.numel() != plan.k * plan.bcols:
+        raise EscsError(ESCS_ERR_ARG, f"B must have k*bCols = {plan.k * plan.bcols} elements")
+    if not isinstance(C, int) and C.numel() != plan.m * plan.bcols:
+        raise EscsError(ESCS_ERR_ARG, f"C must have m*bCols = {plan.m * plan.bcols} elements")
+    if vals is not None and not isinstance(vals, int) and vals.numel() < plan.nnz:
+        raise EscsError(ESCS_ERR_ARG, f"vals must have at least nnz = {plan.nnz} elements")
+    rc = _lib.escs_spmm(plan.handle, _ptr(vals), _ptr(B), _ptr(C), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+def escs_gather_probe(plan: Plan, B, sink, stream=None) -> None:
+    rc = _lib.escs_gather_probe(plan.handle, _ptr(B), _ptr(sink), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+def escs_free(plan: Plan) -> None:
+    plan.close()
+
+
+def escs_plan_export(plan: Plan) -> dict:
+    v = _View()
+    if _lib.escs_plan_export(plan.handle, ctypes.byref(v)) != ESCS_OK:
+        _raise_last()
+    hdr = dict(zip(HEADER_FIELDS, (int(x) for x in v.header)))
+    NG, G, NI, nnz = hdr["NG"], hdr["G"], hdr["n_items"], hdr["nnz"]
+    sizes = {"grp_panel": NG, "grp_mask": NG, "grp_col_ptr": NG + 1, "grp_val_ptr": NG + 1,
+             "gcol": G, "slot_src": nnz, "item_panel": NI, "item_group_begin": NI,
+             "item_gcol_ptr": NI + 1}
+    out = {"header": hdr}
+    for n in PLAN_ARRAYS:
+        cnt = sizes[n]
+        ptr = getattr(v, n)
+        out[n] = np.ctypeslib.as_array(ptr, shape=(cnt,)).copy() if cnt else np.zeros(0, np.int32)
+    return out
+
+
+def escs_plan_info(plan: Plan) -> dict:
+    s = _Stats()
+    if _lib.escs_plan_info(plan.handle, ctypes.byref(s)) != ESCS_OK:
+        _raise_last()
+    return {n: getattr(s, n) for n, _ in _Stats._fields_}
+
+
+def spmm(plan: Plan, vals, B, C=None, stream=None):
+    """Convenience: allocate C if needed (torch), run escs_spmm, return C."""
+    if C is None:
+        import torch
+        C = torch.empty((plan.m, plan.bcols), dtype=torch.float32, device=B.device)
+    escs_spmm(plan, vals, B, C, stream)
+    return C

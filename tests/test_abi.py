@@ -1,0 +1,106 @@
+"""The C-ABI library loads, exports every symbol include/escs.h declares, and
+reports argument/CSR errors as the header documents (no GPU compute here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2506_15174_b200 import escs, synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "escs.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(escs_[a-z_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    lib = ctypes.CDLL(escs.LIB_PATH)
+    names = declared_functions()
+    assert set(names) == set(escs.EXPORTED_SYMBOLS)
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_version():
+    assert "sm_100a" in escs.escs_version()
+
+
+def test_kernels_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", escs.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def plan_err(*args, **kw):
+    with pytest.raises(escs.EscsError) as e:
+        escs.escs_plan_ex(*args, host_only=1, **kw)
+    return e.value.code
+
+
+def test_csr_errors():
+    rp = np.array([0, 2, 3], np.int32)
+    assert plan_err(2, 4, 3, rp, np.array([0, 1, 5], np.int32), 32) == escs.ESCS_ERR_CSR  # range
+    assert plan_err(2, 4, 3, rp, np.array([1, 1, 0], np.int32), 32) == escs.ESCS_ERR_CSR  # dup
+    assert plan_err(2, 4, 3, rp, np.array([1, 0, 0], np.int32), 32) == escs.ESCS_ERR_CSR  # unsorted
+    assert plan_err(2, 4, 3, np.array([1, 2, 3], np.int32), np.array([0, 1, 2], np.int32), 32) \
+        == escs.ESCS_ERR_CSR
+    assert plan_err(2, 4, 3, np.array([0, 2, 1], np.int32), np.array([0, 1, 2], np.int32), 32) \
+        == escs.ESCS_ERR_CSR
+    code, msg = escs.escs_last_error()
+    assert code == escs.ESCS_ERR_CSR and "row" in msg
+
+
+def test_arg_errors():
+    rp = np.array([0, 1], np.int32)
+    ci = np.array([0], np.int32)
+    assert plan_err(0, 1, 0, np.array([0], np.int32), ci, 32) == escs.ESCS_ERR_ARG
+    assert plan_err(1, 1, 1, rp, ci, 0) == escs.ESCS_ERR_ARG
+    assert plan_err(1, 1, 1, rp, ci, 300) == escs.ESCS_ERR_UNSUPPORTED
+    assert plan_err(1, 1, 1, rp, ci, 32, ufi=17) == escs.ESCS_ERR_ARG
+    assert plan_err(1, 1, 1, rp, ci, 32, cta_warps=33) == escs.ESCS_ERR_ARG
+    assert plan_err(1 << 31, 1, 1, rp, ci, 32) == escs.ESCS_ERR_ARG
+
+
+def test_host_only_plan_rejects_spmm():
+    A = synth.config("c1").A
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1)
+    rc = escs._lib.escs_spmm(pl.handle, 16, 16, 16, None)
+    assert rc == escs.ESCS_ERR_ARG
+    assert "host-only" in escs.escs_last_error()[1]
+    assert escs._lib.escs_spmm(None, 16, 16, 16, None) == escs.ESCS_ERR_ARG
+    escs.escs_free(pl)
+    escs._lib.escs_free(None)   # NULL is a no-op
+
+
+def test_plan_info_and_auto_params():
+    A = synth.magnitude_pruned(512, 512, 0.9, 5)
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, host_only=1)
+    info = pl.info
+    assert info["h"] == 4 and info["T"] >= 16 and info["device"] == -1
+    assert info["nnz"] == A.nnz and info["n_tiles"] >= 1 and 1 <= info["cta_warps"] <= 16
+    hdr = pl.export()["header"]
+    assert hdr["T"] == info["T"] and hdr["bCols"] == 64
+
+
+def test_env_params(monkeypatch):
+    A = synth.config("c1").A
+    monkeypatch.setenv("ESCS_PARAMS", "ufi=3,T=9,warps=5")
+    info = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1).info
+    assert (info["h"], info["T"], info["cta_warps"]) == (3, 9, 5)
+
+
+def test_tiles_cover_items():
+    """CTA tiles (device-only schedule) cover every item exactly once; a
+    panel's items never straddle a non-heavy tile boundary."""
+    A = synth.power_law(1024, 1024, 0.98, 3)
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 128, ufi=4, T=16, cta_warps=4,
+                           host_only=1)
+    info = pl.info
+    assert info["n_heavy"] > 0
+    assert info["n_tiles"] >= -(-info["n_items"] // 4)

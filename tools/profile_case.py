@@ -1,0 +1,48 @@
+"""Run one workload problem's escs_spmm a few times (for ncu / quick timing).
+
+    python tools/profile_case.py --shape 2048x512 --s 0.7 --n 128 [--reps 5] [--c4|--c5]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="2048x512")
+    ap.add_argument("--s", type=float, default=0.7)
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--config", default=None, help="c1/c4/c5 instead of a suite shape")
+    ap.add_argument("--probe", action="store_true")
+    a = ap.parse_args()
+    import torch
+    from paper_2506_15174_b200 import escs, synth
+    if a.config:
+        p = synth.config(a.config)
+        A, B = p.A, p.B
+    else:
+        m, k = (int(x) for x in a.shape.split("x"))
+        A = synth.magnitude_pruned(m, k, a.s, 1234)
+        B = synth.dense_b(k, a.n, 99)
+    pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1])
+    print(pl.info, flush=True)
+    dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
+    dC = torch.empty(A.m, B.shape[1], device="cuda")
+    sink = torch.empty(pl.info["n_tiles"] * 32 * pl.info["cta_warps"], device="cuda")
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(a.reps):
+        s.record()
+        if a.probe:
+            escs.escs_gather_probe(pl, dB, sink)
+        else:
+            escs.escs_spmm(pl, dv, dB, dC)
+        e.record()
+        torch.cuda.synchronize()
+        print(f"rep {i}: {s.elapsed_time(e) * 1e3:.1f} us", flush=True)
+
+
+if __name__ == "__main__":
+    main()
