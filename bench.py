@@ -323,7 +323,9 @@ def run_escs(args):
         dev[p.name] = d
         shard_problems.append((p, d))
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
-    stream = torch.cuda.current_stream(device)
+    # all work on one non-default stream (graph capture needs a non-default stream)
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
 
     def step(per_launch=None):
         for i, (p, d) in enumerate(shard_problems):

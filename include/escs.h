@@ -115,9 +115,9 @@ typedef struct {
                              host-only plans, 1..ESCS_MAX_UFI for device plans   */
     int32_t T;            /* max gcols per item (balanced tiles), 0 = auto      */
     int32_t host_only;    /* 1: build host arrays only (no CUDA), for parity     */
-    int32_t cta_warps;    /* warps per CTA tile, 0 = auto, else 1..32            */
+    int32_t cta_warps;    /* warps per CTA tile, 0 = auto, else 1..16            */
     int32_t variant;      /* 0 = auto, 1 = vector (float4) kernel, 2 = scalar    */
-    int32_t ufk;          /* B-row loads in flight per sub-warp (UFk), 0 = auto  */
+    int32_t ufk;          /* B-row loads in flight per warp (UFk: 4 or 8), 0 = auto */
     int32_t nthreads;     /* planner threads, 0 = hardware concurrency           */
     int32_t reserved[5];  /* must be zero                                        */
 } escs_params;

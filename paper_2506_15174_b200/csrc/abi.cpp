@@ -68,18 +68,20 @@ void apply_env(escs::Params& p, bool& set_warps) {
     }
 }
 
-// Warps per CTA tile: a multiple of the typical number of items per panel, so
-// that whole panels fill tiles without idle warps (about 8 warps per CTA).
+// Warps per CTA tile: at least the number of items of all but the heaviest 1%
+// of panels (so they combine inside one CTA), rounded up to a multiple that
+// gives about 8 warps per CTA; at most 16.
 int auto_cta_warps(const escs::PlanHost& ph) {
     const int64_t nP = ph.header[7];
     const int64_t NI = ph.item_panel.size();
     if (nP == 0) return 8;
     std::vector<int32_t> per(nP, 0);
     for (int64_t i = 0; i < NI; i++) per[ph.item_panel[i]]++;
-    std::nth_element(per.begin(), per.begin() + nP / 2, per.end());
-    const int typ = std::max(1, per[nP / 2]);
-    if (typ >= 16) return 16;
-    return std::max(1, typ * std::max(1, 8 / typ));
+    const int64_t k99 = std::min<int64_t>(nP - 1, (nP * 99) / 100);
+    std::nth_element(per.begin(), per.begin() + k99, per.end());
+    const int typ = std::max(1, per[k99]);
+    if (typ >= 8) return std::min(typ, 16);
+    return typ * std::max(1, 8 / typ);
 }
 
 template <class T>
@@ -103,28 +105,35 @@ bool upload(escs_plan_impl* P) {
     auto& ph = P->host;
     auto& dp = P->dev;
     const int h = ph.header[5], n = ph.header[4];
-    const int64_t NG = ph.header[8], G = ph.header[9], NI = ph.header[10], nnz = ph.header[3];
-    // device group records: col_begin, col_end, val_begin, mask
-    std::vector<int32_t> grp(4 * NG), items(4 * NI);
-    for (int64_t g = 0; g < NG; g++) {
-        grp[4 * g + 0] = ph.grp_col_ptr[g];
-        grp[4 * g + 1] = ph.grp_col_ptr[g + 1];
-        grp[4 * g + 2] = ph.grp_val_ptr[g];
-        grp[4 * g + 3] = ph.grp_mask[g];
-    }
-    for (int64_t i = 0; i < NI; i++) {
-        items[4 * i + 0] = ph.item_panel[i];
-        items[4 * i + 1] = ph.item_group_begin[i];
-        items[4 * i + 2] = ph.item_gcol_ptr[i];
-        items[4 * i + 3] = ph.item_gcol_ptr[i + 1];
+    const int64_t NG = ph.header[8], G = ph.header[9], nnz = ph.header[3];
+    // packed gcols (column | pattern << 27) and items {panel, gcol_begin,
+    // gcol_end, slot_begin}: the kernel needs no group records (Reading R1:
+    // a panel's value slots are contiguous in stream order).
+    std::vector<int32_t> gpk(G);
+    for (int64_t g = 0; g < NG; g++)
+        for (int32_t c = ph.grp_col_ptr[g]; c < ph.grp_col_ptr[g + 1]; c++)
+            gpk[c] = ph.gcol[c] | (ph.grp_mask[g] << 27);
+    const int64_t NS = ph.slot_item.size();
+    std::vector<int32_t> items(4 * NS, 0);
+    for (int64_t k = 0; k < NS; k++) {
+        const int32_t i = ph.slot_item[k];
+        if (i < 0) continue;
+        const int32_t gb = ph.item_group_begin[i], s0 = ph.item_gcol_ptr[i];
+        int32_t sb = 0;
+        if (gb < NG)
+            sb = ph.grp_val_ptr[gb] +
+                 (s0 - ph.grp_col_ptr[gb]) * __builtin_popcount((unsigned)ph.grp_mask[gb]);
+        items[4 * k + 0] = ph.item_panel[i];
+        items[4 * k + 1] = s0;
+        items[4 * k + 2] = ph.item_gcol_ptr[i + 1];
+        items[4 * k + 3] = sb;
     }
     size_t off = 0;
-    const size_t o_grp = add_region<int32_t>(off, 4 * NG);
-    const size_t o_gcol = add_region<int32_t>(off, G);
+    const size_t o_gpk = add_region<int32_t>(off, G);
     const size_t o_slot = add_region<int32_t>(off, nnz);
-    const size_t o_items = add_region<int32_t>(off, 4 * NI);
-    const size_t o_aux = add_region<int32_t>(off, NI);
-    const size_t o_tiles = add_region<int32_t>(off, ph.tile_info.size());
+    const size_t o_items = add_region<int32_t>(off, 4 * NS);
+    const size_t o_aux = add_region<int32_t>(off, NS);
+    const size_t o_tiles = add_region<int32_t>(off, ph.tile_heavy.size());
     const size_t o_heavy = add_region<int32_t>(off, ph.heavy_info.size());
     const size_t o_cnt = add_region<int32_t>(off, ph.n_heavy);
     const size_t ws_elems = (size_t)ph.n_heavy_tiles * h * n;
@@ -146,20 +155,18 @@ bool upload(escs_plan_impl* P) {
         CUDA_TRY(cudaMemcpy(b + o, src, bytes, cudaMemcpyHostToDevice));
         return true;
     };
-    if (!put(o_grp, grp.data(), grp.size() * 4)) return false;
-    if (!put(o_gcol, ph.gcol.data(), G * 4)) return false;
+    if (!put(o_gpk, gpk.data(), G * 4)) return false;
     if (!put(o_slot, ph.slot_src.data(), nnz * 4)) return false;
     if (!put(o_items, items.data(), items.size() * 4)) return false;
-    if (!put(o_aux, ph.item_aux.data(), NI * 4)) return false;
-    if (!put(o_tiles, ph.tile_info.data(), ph.tile_info.size() * 4)) return false;
+    if (!put(o_aux, ph.slot_aux.data(), NS * 4)) return false;
+    if (!put(o_tiles, ph.tile_heavy.data(), ph.tile_heavy.size() * 4)) return false;
     if (!put(o_heavy, ph.heavy_info.data(), ph.heavy_info.size() * 4)) return false;
     if (ph.n_heavy) CUDA_TRY(cudaMemset(b + o_cnt, 0, ph.n_heavy * 4));
-    dp.grp = reinterpret_cast<const int32_t*>(b + o_grp);
-    dp.gcol = reinterpret_cast<const int32_t*>(b + o_gcol);
+    dp.gpk = reinterpret_cast<const int32_t*>(b + o_gpk);
     dp.slot = reinterpret_cast<const int32_t*>(b + o_slot);
     dp.items = reinterpret_cast<const int32_t*>(b + o_items);
     dp.item_aux = reinterpret_cast<const int32_t*>(b + o_aux);
-    dp.tiles = reinterpret_cast<const int32_t*>(b + o_tiles);
+    dp.tile_heavy = reinterpret_cast<const int32_t*>(b + o_tiles);
     dp.heavy = reinterpret_cast<const int32_t*>(b + o_heavy);
     dp.counters = reinterpret_cast<int32_t*>(b + o_cnt);
     dp.ws = reinterpret_cast<float*>(b + o_ws);
@@ -221,6 +228,10 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
         return nullptr;
     }
     if (p.variant == 1 && !(bCols == 32 || bCols == 64 || bCols == 128 || bCols == 256)) p.variant = 2;
+    if (!host_only && k >= (1 << 27)) {
+        fail(ESCS_ERR_UNSUPPORTED, "device plans need k < 2^27 (packed column words)");
+        return nullptr;
+    }
     if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk)) {
         fail(ESCS_ERR_UNSUPPORTED, "no kernel for ufi=" + std::to_string(p.h) + " bCols=" +
                                        std::to_string(bCols) + " variant=" +

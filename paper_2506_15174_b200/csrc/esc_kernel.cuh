@@ -1,21 +1,24 @@
 // esc_kernel.cuh -- the enumerate-and-sparse-coarsen SpMM kernel for sm_100a.
 //
 // Paper mapping (arXiv 2506.15174):
-//   * enumeration (§3.2): a warp works on one item of one row panel
-//     (UFi = H rows); inside the item, every group (panel, pattern) is a run of
-//     columns sharing one UFi-bit pattern, dispatched once to a body
-//     specialised for that pattern, so the hot loop has no data-dependent
-//     conditionals (the "enumerated blocks" of Listing 4);
-//   * thread mapping map(j, W) (§3.3.1): lanes own consecutive
-//     columns of B/C (float4 per lane on the vector map, 32-strided scalars on
-//     the scalar map = the paper's WarpTile mapping, Listing 5);
+//   * enumeration (§3.2): a warp works on one item (a balanced
+//     slice of one UFi = H row panel's column stream).  The stream is sorted by
+//     pattern, so consecutive columns share one UFi-bit pattern; every column
+//     runs the enumerated block of its pattern (Listing 4): the
+//     pattern is warp-uniform, its bits predicate the row FMAs, so exactly
+//     popcount(pattern) rows accumulate and no lane diverges;
+//   * thread mapping map(j, W) (§3.3.1): the 32 lanes own the
+//     bCols columns of B/C (F consecutive floats per lane on the vector map,
+//     32-strided scalars on the scalar map = the paper's WarpTile mapping);
 //   * thread coarsening (§3.3.2): each lane keeps H x F
 //     accumulators (pattern rows x its columns); a B element loaded once into a
 //     register is reused for every row of the pattern, an A value for all the
-//     lane's columns; UFK gathered B rows are in flight per sub-warp;
-//   * data transformation (§3.3.3): columns ("Cols") and value
-//     slots ("ANNZ" order, Reading R1) are staged 32 at a time by the warp with
-//     coalesced loads and broadcast with __shfl_sync;
+//     lane's columns; columns are processed in batches of UFK gathered B rows
+//     in flight per warp;
+//   * data transformation (§3.3.3): columns ("Cols", packed with
+//     their pattern) and value slots ("ANNZ" order, Reading R1) are staged 32
+//     at a time by the warp with coalesced loads, one chunk ahead, and
+//     broadcast with __shfl_sync;
 //   * safety: write-after-write between items of one panel is
 //     resolved by a deterministic combine -- shared memory inside the CTA
 //     tile, a global workspace + counter (last arriver sums in tile order)
@@ -29,14 +32,15 @@ namespace escs {
 namespace kern {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kColBits = 27;                       // packed gcol: col | mask << 27
+constexpr int kColMask = (1 << kColBits) - 1;
 
 struct KParams {
-    const int4* __restrict__ grp;      // col_begin, col_end, val_begin, mask
-    const int* __restrict__ gcol;
-    const int* __restrict__ slot;
-    const int4* __restrict__ items;    // panel, group_begin, gcol_begin, gcol_end
-    const int* __restrict__ item_aux;  // lead | cnt << 8
-    const int4* __restrict__ tiles;    // item_begin, item_end, heavy_id, flags
+    const int* __restrict__ gpk;       // packed gcols: column | pattern << 27
+    const int* __restrict__ slot;      // value slot -> CSR position
+    const int4* __restrict__ items;    // per slot: panel, gcol_begin, gcol_end, slot_begin
+    const int* __restrict__ item_aux;  // per slot: lead | cnt<<8 | active<<16 | sync<<17 | heavy<<18
+    const int2* __restrict__ tile_heavy; // per tile: heavy id, ordinal (heavy tiles only)
     const int4* __restrict__ heavy;    // panel, ws_base, ntiles, 0
     float* ws;
     int* counters;
@@ -46,161 +50,191 @@ struct KParams {
     int m, n;
 };
 
-__device__ __forceinline__ float4 ldg_f4(const float4* p) {
-    float4 r;
-    asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-}
-__device__ __forceinline__ int ldg_stream(const int* p) {
+__device__ __forceinline__ int ld_stream(const int* p) {
     int r;
     asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 
-// Lane map with float4 lanes: L lanes cover one B row of N = 4*V*L floats,
-// S = 32/L sub-warps process S gathered rows per warp step.
-template <int L_, int V_>
+// Vector lane map: N = 32*F, lane owns columns [lane*F, lane*F + F).
+template <int F_>
 struct VecMap {
-    static constexpr int L = L_, S = 32 / L_, V = V_, F = 4 * V_;
+    static constexpr int F = F_;
     static constexpr bool kVec = true;
-    __device__ static __forceinline__ int col(int lj, int f) { return (lj * V + (f >> 2)) * 4 + (f & 3); }
-    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lj) {
-        const float4* r4 = reinterpret_cast<const float4*>(row) + lj * V;
+    __device__ static __forceinline__ int col(int lane, int f) { return lane * F + f; }
+    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lane) {
+        const float* q = row + lane * F;
+        if constexpr (F == 1) {
+            asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(b[0]) : "l"(q));
+        } else if constexpr (F == 2) {
+            asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(b[0]), "=f"(b[1]) : "l"(q));
+        } else {
 #pragma unroll
-        for (int v = 0; v < V; v++) {
-            const float4 x = ldg_f4(r4 + v);
-            b[4 * v + 0] = x.x; b[4 * v + 1] = x.y; b[4 * v + 2] = x.z; b[4 * v + 3] = x.w;
+            for (int v = 0; v < F / 4; v++)
+                asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(b[4 * v]), "=f"(b[4 * v + 1]), "=f"(b[4 * v + 2]),
+                               "=f"(b[4 * v + 3])
+                             : "l"(q + 4 * v));
         }
     }
-    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lj) {
-        float4* r4 = reinterpret_cast<float4*>(row) + lj * V;
+    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lane) {
+        float* q = row + lane * F;
+        if constexpr (F == 1) {
+            q[0] = a[0];
+        } else if constexpr (F == 2) {
+            *reinterpret_cast<float2*>(q) = make_float2(a[0], a[1]);
+        } else {
 #pragma unroll
-        for (int v = 0; v < V; v++)
-            r4[v] = make_float4(a[4 * v + 0], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+            for (int v = 0; v < F / 4; v++)
+                reinterpret_cast<float4*>(q)[v] =
+                    make_float4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
+        }
     }
 };
 
-// Scalar lane map (the paper's map(j, 32*WarpTile), Listing 5/6): lane owns
+// Scalar lane map (the paper's map(j, 32*WarpTile), Listings 5-6): lane owns
 // columns lane + 32*f, f < WT, predicated on j < N.  Any N <= 32*WT, any
 // alignment.
 template <int WT>
 struct ScalarMap {
-    static constexpr int L = 32, S = 1, V = 0, F = WT;
+    static constexpr int F = WT;
     static constexpr bool kVec = false;
-    __device__ static __forceinline__ int col(int lj, int f) { return lj + 32 * f; }
-    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int n, int lj) {
+    __device__ static __forceinline__ int col(int lane, int f) { return lane + 32 * f; }
+    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int n, int lane) {
 #pragma unroll
         for (int f = 0; f < F; f++) {
-            const int j = lj + 32 * f;
+            const int j = lane + 32 * f;
             b[f] = (j < n) ? __ldg(row + j) : 0.f;
         }
     }
-    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int n, int lj) {
+    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int n, int lane) {
 #pragma unroll
         for (int f = 0; f < F; f++) {
-            const int j = lj + 32 * f;
+            const int j = lane + 32 * f;
             if (j < n) row[j] = a[f];
         }
     }
 };
 
-// One run of columns [pos, gend) of a group with pattern MASK.  The values of
-// column ordinal ci sit at slots vbase + ci*P + rank (Reading R1).
-template <int H, int MASK, class Map, int UFK, bool PROBE>
-__device__ __forceinline__ void run_group(const KParams& p, float (&acc)[H][Map::F], int cbeg,
-                                          int vbase, int pos, int gend, int lane, int sub, int lj) {
-    constexpr int P = __builtin_popcount(MASK);
-    constexpr int S = Map::S, F = Map::F;
-    for (int c0 = pos; c0 < gend; c0 += 32) {
-        const int n = min(32, gend - c0);
-        const int myc = c0 + lane;
-        int col = 0;
-        float v[P];
-        if (lane < n) {
-            col = ldg_stream(p.gcol + myc);
-            if constexpr (!PROBE) {
-                const int* sp = p.slot + vbase + (myc - cbeg) * P;
+// Stage the values of one 32-column chunk: lane l holds, for its column, the
+// value of every pattern row r in w[r] (0 for rows outside the pattern),
+// read through the slot map.  Slots of a panel's stream are contiguous in
+// stream order with popcount(mask) slots per column, pattern rows ascending
+// (Reading R1), so the lane's first slot is the chunk base plus an exclusive
+// warp scan of the popcounts.
+template <int H>
+__device__ __forceinline__ int stage_values(const KParams& p, int pk, int sbase, float (&w)[H],
+                                            int lane) {
+    const unsigned mask = (unsigned)pk >> kColBits;
+    const unsigned lt = (1u << lane) - 1u;
+    int excl = 0, total = 0;
 #pragma unroll
-                for (int r = 0; r < P; r++) v[r] = __ldg(p.vals + ldg_stream(sp + r));
-            }
+    for (int bit = 0; bit < 3; bit++) {
+        const unsigned bal = __ballot_sync(kFull, (__popc(mask) >> bit) & 1);
+        excl += __popc(bal & lt) << bit;
+        total += __popc(bal) << bit;
+    }
+    const int* sp = p.slot + sbase + excl;
+#pragma unroll
+    for (int r = 0; r < H; r++) {
+        const int rank = __popc(mask & ((1u << r) - 1u));
+        w[r] = ((mask >> r) & 1u) ? __ldg(p.vals + ld_stream(sp + rank)) : 0.f;
+    }
+    return sbase + total;
+}
+
+// Walk one item: columns [beg, end) of the gcol stream, values from sbase.
+// Columns are processed in batches of U: U gathered B rows in flight (thread
+// coarsening over k, "UFk"), then for every column the rows of its
+// pattern accumulate a*b -- the enumerated block of Listing 4,
+// realised as warp-uniform predicates on the pattern bits (the pattern is the
+// same for all lanes), so structural zeros are never multiplied and the code
+// stays one compact body for all 2^UFi - 1 patterns.
+template <int H, class Map, int U, bool PROBE>
+__device__ __forceinline__ void walk(const KParams& p, int beg, int end, int sbase,
+                                     float (&acc)[H][Map::F], int lane) {
+    constexpr int F = Map::F;
+    static_assert(32 % U == 0, "UFK must divide 32");
+    const int n = end - beg;
+    const int* gp = p.gpk + beg;
+    int pk0 = (lane < n) ? ld_stream(gp + lane) : 0;
+    int pk1 = (32 + lane < n) ? ld_stream(gp + 32 + lane) : 0;
+    float v0[H], v1[H];
+    if constexpr (!PROBE) {
+        sbase = stage_values<H>(p, pk0, sbase, v0, lane);
+    } else {
+#pragma unroll
+        for (int j = 0; j < H; j++) v0[j] = 0.f;
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        // one chunk ahead: packed words of chunk+1 are in pk1; stage its values
+        int pk2 = 0;
+        if (c0 + 32 < n) {
+            pk2 = (c0 + 64 + lane < n) ? ld_stream(gp + c0 + 64 + lane) : 0;
+            if constexpr (!PROBE) sbase = stage_values<H>(p, pk1, sbase, v1, lane);
         }
-        if (PROBE || lane >= n) {
+        const int cn = min(32, n - c0);
+        // columns past the item end have pk = 0: row 0 is loaded, pattern 0
+        // predicates every FMA off
+#pragma unroll 1
+        for (int s = 0; s < cn; s += U) {
+            float b[U][F];
+            int pq[U];
 #pragma unroll
-            for (int r = 0; r < P; r++) v[r] = 0.f;
-        }
-        for (int t = 0; t < n; t += S * UFK) {
-            float b[UFK][F];
-            float a[UFK][P];
-#pragma unroll
-            for (int u = 0; u < UFK; u++) {
-                const int tt = t + u * S + sub;
-                const int src = tt & 31;
-                const int cc = __shfl_sync(kFull, col, src);
-#pragma unroll
-                for (int r = 0; r < P; r++) a[u][r] = __shfl_sync(kFull, v[r], src);
-                if (tt < n) {
-                    Map::load(b[u], p.B + (size_t)cc * p.n, p.n, lj);
-                } else {
-#pragma unroll
-                    for (int f = 0; f < F; f++) b[u][f] = 0.f;
-                }
+            for (int u = 0; u < U; u++) {
+                pq[u] = __shfl_sync(kFull, pk0, s + u);
+                Map::load(b[u], p.B + (size_t)(pq[u] & kColMask) * p.n, p.n, lane);
             }
 #pragma unroll
-            for (int u = 0; u < UFK; u++) {
+            for (int u = 0; u < U; u++) {
+                const unsigned mk = (unsigned)pq[u] >> kColBits;
                 if constexpr (PROBE) {
 #pragma unroll
-                    for (int f = 0; f < F; f++) acc[0][f] += b[u][f];
+                    for (int f = 0; f < F; f++)
+                        if (mk) acc[0][f] += b[u][f];
                 } else {
-                    int rank = 0;
 #pragma unroll
                     for (int row = 0; row < H; row++) {
-                        if ((MASK >> row) & 1) {
+                        const float a = __shfl_sync(kFull, v0[row], s + u);
+                        const bool on = (mk >> row) & 1u;
 #pragma unroll
-                            for (int f = 0; f < F; f++)
-                                acc[row][f] = fmaf(a[u][rank], b[u][f], acc[row][f]);
-                            rank++;
-                        }
+                        for (int f = 0; f < F; f++)
+                            if (on) acc[row][f] = fmaf(a, b[u][f], acc[row][f]);
                     }
                 }
             }
         }
-    }
-}
-
-// Warp-uniform pattern switch (one specialised body per enumerated block).
-template <int H, class Map, int UFK, bool PROBE, int M = 1>
-__device__ __forceinline__ void dispatch_mask(int mask, const KParams& p, float (&acc)[H][Map::F],
-                                              int cbeg, int vbase, int pos, int gend, int lane,
-                                              int sub, int lj) {
-    if constexpr (M < (1 << H)) {
-        if (mask == M)
-            run_group<H, M, Map, UFK, PROBE>(p, acc, cbeg, vbase, pos, gend, lane, sub, lj);
-        else
-            dispatch_mask<H, Map, UFK, PROBE, M + 1>(mask, p, acc, cbeg, vbase, pos, gend, lane,
-                                                     sub, lj);
+        pk0 = pk1;
+        pk1 = pk2;
+#pragma unroll
+        for (int j = 0; j < H; j++) v0[j] = v1[j];
     }
 }
 
 template <int H, class Map>
 __device__ __forceinline__ void store_rows(const KParams& p, int panel, const float (&a)[H][Map::F],
-                                           int sub, int lj) {
+                                           int lane) {
 #pragma unroll
     for (int r = 0; r < H; r++) {
         const int row = panel * H + r;
-        if ((r % Map::S) == sub && row < p.m) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
+        if (row < p.m) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lane);
     }
 }
 
-template <int H, class Map, int UFK, bool PROBE>
-__global__ void __launch_bounds__(512) esc_spmm_kernel(KParams p) {
-    extern __shared__ float red[];   // [W][H][n] partials of split panels
-    constexpr int F = Map::F, S = Map::S, L = Map::L;
-    const int4 ti = p.tiles[blockIdx.x];
+// Item slots are tile-major: CTA b owns slots [b*W, b*W + W), W = warps per
+// CTA; slot aux = lead | cnt << 8 | active << 16 | tile_sync << 17 |
+// tile_heavy << 18 (lead: warp of the panel's first item in this tile, cnt:
+// the panel's items in this tile).
+template <int H, class Map, int U, bool PROBE>
+__global__ void __launch_bounds__(512, 2) esc_spmm_kernel(KParams p) {
+    extern __shared__ __align__(16) float smem[];   // [W][H][32F] partials of split panels
+    constexpr int F = Map::F;
+    constexpr int WS = H * 32 * F;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sub = lane / L, lj = lane % L;
-    const int item = ti.x + w;
-    const bool active = item < ti.y;
+    const int slot = blockIdx.x * (blockDim.x >> 5) + w;
+    const int aux = p.item_aux[slot];
+    const bool active = (aux >> 16) & 1;
 
     float acc[H][F];
 #pragma unroll
@@ -208,29 +242,11 @@ __global__ void __launch_bounds__(512) esc_spmm_kernel(KParams p) {
 #pragma unroll
         for (int f = 0; f < F; f++) acc[r][f] = 0.f;
 
-    int panel = 0, aux = 0;
+    int panel = 0;
     if (active) {
-        const int4 it = p.items[item];
-        aux = p.item_aux[item];
+        const int4 it = p.items[slot];
         panel = it.x;
-        int g = it.y, pos = it.z;
-        const int end = it.w;
-        while (pos < end) {
-            const int4 gi = p.grp[g];
-            const int gend = min(end, gi.y);
-            dispatch_mask<H, Map, UFK, PROBE>(gi.w, p, acc, gi.x, gi.z, pos, gend, lane, sub, lj);
-            pos = gend;
-            ++g;
-        }
-        if constexpr (S > 1) {   // warp-level reduction of the sub-warps
-#pragma unroll
-            for (int r = 0; r < H; r++)
-#pragma unroll
-                for (int f = 0; f < F; f++)
-#pragma unroll
-                    for (int off = L; off < 32; off <<= 1)
-                        acc[r][f] += __shfl_xor_sync(kFull, acc[r][f], off);
-        }
+        walk<H, Map, U, PROBE>(p, it.y, it.z, it.w, acc, lane);
     }
 
     if constexpr (PROBE) {
@@ -243,78 +259,84 @@ __global__ void __launch_bounds__(512) esc_spmm_kernel(KParams p) {
         return;
     } else {
         const int n = p.n;
-        const bool heavy = ti.z >= 0;
-        const int cnt = aux >> 8, lead = aux & 0xff;
-        if (!(ti.w & 1)) {   // every panel of this tile has exactly one item here
-            if (active) store_rows<H, Map>(p, panel, acc, sub, lj);
+        const bool heavy = (aux >> 18) & 1;
+        const int cnt = (aux >> 8) & 0xff, lead = aux & 0xff;
+        if (!((aux >> 17) & 1)) {   // every panel of this tile has exactly one item here
+            if (active) store_rows<H, Map>(p, panel, acc, lane);
             return;
         }
-        float* mine = red + (size_t)w * H * n;
+        float* mine = smem + (size_t)w * WS;
         if (active && (cnt > 1 || heavy)) {
 #pragma unroll
             for (int r = 0; r < H; r++)
-                if ((r % S) == sub)
 #pragma unroll
-                    for (int f = 0; f < F; f++) {
-                        const int j = Map::col(lj, f);
-                        if (Map::kVec || j < n) mine[r * n + j] = acc[r][f];
-                    }
+                for (int f = 0; f < F; f++) {
+                    const int j = Map::col(lane, f);
+                    if (Map::kVec || j < n) mine[r * 32 * F + j] = acc[r][f];
+                }
         }
         __syncthreads();
         if (!active) return;
         if (cnt == 1 && !heavy) {
-            store_rows<H, Map>(p, panel, acc, sub, lj);
+            store_rows<H, Map>(p, panel, acc, lane);
             return;
         }
         if (w != lead) return;
         // combine the panel's partials in item order (deterministic)
-        float tot[H][F];
+#pragma unroll
+        for (int r = 0; r < H; r++)
+#pragma unroll
+            for (int f = 0; f < F; f++) acc[r][f] = 0.f;
+#pragma unroll 1
+        for (int q = 0; q < cnt; q++) {
+            const float* part = smem + (size_t)(lead + q) * WS;
+#pragma unroll
+            for (int r = 0; r < H; r++)
+#pragma unroll
+                for (int f = 0; f < F; f++) {
+                    const int j = Map::col(lane, f);
+                    if (Map::kVec || j < n) acc[r][f] += part[r * 32 * F + j];
+                }
+        }
+        if (!heavy) {
+            store_rows<H, Map>(p, panel, acc, lane);
+            return;
+        }
+        // heavy panel: its tiles combine through the global workspace
+        const int2 th = p.tile_heavy[blockIdx.x];      // heavy id, ordinal
+        const int4 hv = p.heavy[th.x];                  // panel, ws_base, ntiles
+        float* wsq = p.ws + (size_t)(hv.y + th.y) * H * n;
 #pragma unroll
         for (int r = 0; r < H; r++)
 #pragma unroll
             for (int f = 0; f < F; f++) {
-                const int j = Map::col(lj, f);
-                float s = 0.f;
-                if (Map::kVec || j < n)
-                    for (int q = 0; q < cnt; q++) s += red[((size_t)(lead + q) * H + r) * n + j];
-                tot[r][f] = s;
+                const int j = Map::col(lane, f);
+                if (Map::kVec || j < n) __stcg(wsq + r * n + j, acc[r][f]);
             }
-        if (!heavy) {
-            store_rows<H, Map>(p, panel, tot, sub, lj);
-            return;
-        }
-        // heavy panel: tiles combine through the global workspace
-        const int4 hv = p.heavy[ti.z];
-        const int q = ti.w >> 1;
-        float* wsq = p.ws + (size_t)(hv.y + q) * H * n;
-#pragma unroll
-        for (int r = 0; r < H; r++)
-            if ((r % S) == sub)
-#pragma unroll
-                for (int f = 0; f < F; f++) {
-                    const int j = Map::col(lj, f);
-                    if (Map::kVec || j < n) __stcg(wsq + r * n + j, tot[r][f]);
-                }
         __threadfence();
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = (atomicAdd(p.counters + ti.z, 1) == hv.z - 1);
+        if (lane == 0) last = (atomicAdd(p.counters + th.x, 1) == hv.z - 1);
         last = __shfl_sync(kFull, last, 0);
         if (!last) return;
         __threadfence();
 #pragma unroll
         for (int r = 0; r < H; r++)
 #pragma unroll
-            for (int f = 0; f < F; f++) {
-                const int j = Map::col(lj, f);
-                float s = 0.f;
-                if (Map::kVec || j < n)
-                    for (int t = 0; t < hv.z; t++)
-                        s += __ldcg(p.ws + ((size_t)(hv.y + t) * H + r) * n + j);
-                tot[r][f] = s;
-            }
-        store_rows<H, Map>(p, hv.x, tot, sub, lj);
-        if (lane == 0) p.counters[ti.z] = 0;   // self-reset: graph replay safe
+            for (int f = 0; f < F; f++) acc[r][f] = 0.f;
+#pragma unroll 1
+        for (int t = 0; t < hv.z; t++) {
+            const float* part = p.ws + (size_t)(hv.y + t) * H * n;
+#pragma unroll
+            for (int r = 0; r < H; r++)
+#pragma unroll
+                for (int f = 0; f < F; f++) {
+                    const int j = Map::col(lane, f);
+                    if (Map::kVec || j < n) acc[r][f] += __ldcg(part + r * n + j);
+                }
+        }
+        store_rows<H, Map>(p, hv.x, acc, lane);
+        if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
     }
 }
 

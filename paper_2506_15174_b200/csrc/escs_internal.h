@@ -23,11 +23,11 @@ struct PlanHost {
     int32_t header[11] = {0};
     std::vector<int32_t> grp_panel, grp_mask, grp_col_ptr, grp_val_ptr, gcol, slot_src;
     std::vector<int32_t> item_panel, item_group_begin, item_gcol_ptr;
-    // derived (not part of plan parity; deterministic)
-    std::vector<int32_t> item_aux;    // lead | cnt << 8  (warp slot of the panel's first
-                                      // item inside the tile, #items of the panel there)
-    std::vector<int32_t> tile_info;   // 4 per tile: item_begin, item_end, heavy_id, flags
-                                      // flags: bit0 needs_sync, bits 1.. = ordinal q
+    // derived CTA-tile schedule (not part of plan parity; deterministic):
+    // W item slots per tile, tile-major
+    std::vector<int32_t> slot_item;   // canonical item of each slot, -1 = empty
+    std::vector<int32_t> slot_aux;    // lead | cnt<<8 | active<<16 | tile_sync<<17 | tile_heavy<<18
+    std::vector<int32_t> tile_heavy;  // 2 per tile: heavy id (-1), ordinal
     std::vector<int32_t> heavy_info;  // 4 per heavy panel: panel, ws_base, ntiles, 0
     int n_tiles = 0, n_heavy = 0, n_heavy_tiles = 0, n_split_items = 0;
     bool any_sync = false;
@@ -50,12 +50,11 @@ void build_tiles(PlanHost& ph, int cta_warps);
 
 // Device-side view used by the kernels.
 struct DevPlan {
-    const int32_t* grp = nullptr;       // int4[NG]: col_begin, col_end, val_begin, mask
-    const int32_t* gcol = nullptr;      // int32[G]
+    const int32_t* gpk = nullptr;       // int32[G]: column | pattern << 27
     const int32_t* slot = nullptr;      // int32[nnz]
-    const int32_t* items = nullptr;     // int4[n_items]: panel, group_begin, gcol_begin, gcol_end
-    const int32_t* item_aux = nullptr;  // int32[n_items]
-    const int32_t* tiles = nullptr;     // int4[n_tiles]
+    const int32_t* items = nullptr;     // int4[n_slots]: panel, gcol_begin, gcol_end, slot_begin
+    const int32_t* item_aux = nullptr;  // int32[n_slots]
+    const int32_t* tile_heavy = nullptr;  // int2[n_tiles]
     const int32_t* heavy = nullptr;     // int4[n_heavy]
     float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
     int32_t* counters = nullptr;        // int32[n_heavy]

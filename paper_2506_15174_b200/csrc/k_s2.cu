@@ -1,13 +1,17 @@
-// Instantiations of the ESC kernel for lane map ScalarMap<2> (generated list; see esc_kernel.cuh).
+// Instantiations of the ESC kernel for lane map ScalarMap<2> (see esc_kernel.cuh).
 #include "esc_kernel.cuh"
 namespace escs {
 namespace kern {
 KernelFn get_s2(int h, int ufk, bool probe) {
     using M = ScalarMap<2>;
     if (h == 1 && ufk == 4 && !probe) return esc_spmm_kernel<1, M, 4, false>;
+    if (h == 1 && ufk == 8 && !probe) return esc_spmm_kernel<1, M, 8, false>;
     if (h == 2 && ufk == 4 && !probe) return esc_spmm_kernel<2, M, 4, false>;
+    if (h == 2 && ufk == 8 && !probe) return esc_spmm_kernel<2, M, 8, false>;
     if (h == 3 && ufk == 4 && !probe) return esc_spmm_kernel<3, M, 4, false>;
+    if (h == 3 && ufk == 8 && !probe) return esc_spmm_kernel<3, M, 8, false>;
     if (h == 4 && ufk == 4 && !probe) return esc_spmm_kernel<4, M, 4, false>;
+    if (h == 4 && ufk == 8 && !probe) return esc_spmm_kernel<4, M, 8, false>;
     return nullptr;
 }
 }  // namespace kern

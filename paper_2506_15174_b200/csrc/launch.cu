@@ -29,21 +29,20 @@ kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
         }
     }
     if (probe) return nullptr;
-    if (n <= 32) return kern::get_s1(h, 4, false);
-    if (n <= 64) return kern::get_s2(h, 4, false);
-    if (n <= 128) return kern::get_s4(h, 4, false);
-    if (n <= 256) return kern::get_s8(h, 4, false);
+    if (n <= 32) return kern::get_s1(h, ufk, false);
+    if (n <= 64) return kern::get_s2(h, ufk, false);
+    if (n <= 128) return kern::get_s4(h, ufk, false);
+    if (n <= 256) return kern::get_s8(h, ufk, false);
     return nullptr;
 }
 
 kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C) {
     kern::KParams p;
-    p.grp = reinterpret_cast<const int4*>(dp.grp);
-    p.gcol = dp.gcol;
+    p.gpk = dp.gpk;
     p.slot = dp.slot;
     p.items = reinterpret_cast<const int4*>(dp.items);
     p.item_aux = dp.item_aux;
-    p.tiles = reinterpret_cast<const int4*>(dp.tiles);
+    p.tile_heavy = reinterpret_cast<const int2*>(dp.tile_heavy);
     p.heavy = reinterpret_cast<const int4*>(dp.heavy);
     p.ws = dp.ws;
     p.counters = dp.counters;
@@ -59,39 +58,44 @@ kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, 
 
 bool kernel_supported(int h, int bcols, int variant, int ufk) {
     if (h < 1 || h > 4 || bcols < 1 || bcols > 256) return false;
-    const bool vec = variant == 1;
-    if (vec) return select_kernel(h, bcols, true, ufk, false) != nullptr;
-    return select_kernel(h, bcols, false, 4, false) != nullptr;
+    return select_kernel(h, bcols, variant == 1, ufk, false) != nullptr &&
+           select_kernel(h, bcols, false, ufk, false) != nullptr;
 }
 
-size_t smem_bytes(const DevPlan& dp) {
-    if (!dp.any_sync) return 0;
-    return (size_t)dp.cta_warps * dp.h * dp.bcols * sizeof(float);
+// floats per lane-column slot F of the lane map the launch will use
+static int lane_floats(int n, bool vec) {
+    if (vec) return n / 32;
+    return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
 }
+
+static size_t smem_for(const DevPlan& dp, bool vec) {
+    const int F = lane_floats(dp.bcols, vec);
+    if (!dp.any_sync) return 0;
+    return (size_t)dp.cta_warps * dp.h * 32 * F * sizeof(float);
+}
+
+size_t smem_bytes(const DevPlan& dp) { return smem_for(dp, dp.variant == 1); }
 
 int prepare_kernels(const DevPlan& dp) {
-    const size_t smem = smem_bytes(dp);
+    // Kernel attributes are per function and shared by every plan: only ever
+    // raise the dynamic shared memory limit (never lower it under another plan).
     for (int vec = 0; vec < 2; vec++) {
         if (vec && dp.variant != 1) continue;
-        kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec == 1, vec ? dp.ufk : 4, false);
+        const size_t smem = smem_for(dp, vec == 1);
+        if (smem <= 48 * 1024) continue;
+        kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec == 1, dp.ufk, false);
         if (!fn) continue;
-        cudaError_t e = cudaFuncSetAttribute((const void*)fn,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaFuncAttributes attr;
+        cudaError_t e = cudaFuncGetAttributes(&attr, (const void*)fn);
         if (e != cudaSuccess) return (int)e;
-        // prefer L1 for the gathered B rows; leave enough carveout for the
-        // combine buffers of resident tiles
-        const int threads = 32 * dp.cta_warps;
-        const int ctas = 2048 / threads;
-        int pct = (int)((smem * ctas * 100 + 228 * 1024 - 1) / (228 * 1024));
-        if (pct > 100) pct = 100;
-        e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 pct);
+        if ((size_t)attr.maxDynamicSharedSizeBytes >= smem) continue;
+        e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
         if (e != cudaSuccess) return (int)e;
         if (vec) {
             kern::KernelFn pf = select_kernel(dp.h, dp.bcols, true, dp.ufk, true);
             if (pf) cudaFuncSetAttribute((const void*)pf,
-                                         cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         }
     }
     return 0;
@@ -100,11 +104,11 @@ int prepare_kernels(const DevPlan& dp) {
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
                 bool vec_ok) {
     const bool vec = vec_ok && dp.variant == 1;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, vec ? dp.ufk : 4, false);
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, vals, B, C);
-    fn<<<dp.n_tiles, 32 * dp.cta_warps, smem_bytes(dp), (cudaStream_t)stream>>>(p);
+    fn<<<dp.n_tiles, 32 * dp.cta_warps, smem_for(dp, vec), (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 
@@ -114,7 +118,7 @@ int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, b
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, nullptr, B, sink);
-    fn<<<dp.n_tiles, 32 * dp.cta_warps, 0, (cudaStream_t)stream>>>(p);
+    fn<<<dp.n_tiles, 32 * dp.cta_warps, smem_for(dp, true), (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 

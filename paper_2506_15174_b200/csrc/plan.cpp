@@ -236,32 +236,45 @@ void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr, const 
 }
 
 // CTA tiles: whole panels are packed greedily (in panel order) into tiles of
-// at most W items, so that a panel split into several items is combined in
+// W item slots, so that a panel split into several items is combined in
 // shared memory by one CTA.  A panel with more than W items ("heavy", the
 // power-law case C4) gets ceil(n/W) exclusive tiles that are combined through
 // a global workspace in tile order (deterministic fixup).
 void build_tiles(PlanHost& ph, int W) {
     const int64_t NI = ph.item_panel.size();
     const int64_t nP = ph.header[7];
-    ph.item_aux.assign(NI, 0);
-    ph.tile_info.clear();
+    ph.slot_item.clear();
+    ph.slot_aux.clear();
+    ph.tile_heavy.clear();
     ph.heavy_info.clear();
     ph.n_heavy = ph.n_heavy_tiles = ph.n_split_items = 0;
     ph.any_sync = false;
-    int64_t cur_begin = 0, cur_end = 0;
+    std::vector<int32_t> lc(NI, 0);      // lead | cnt << 8 per item
+    std::vector<int64_t> cur;            // items of the open tile
     bool cur_sync = false;
-    auto close = [&]() {
-        if (cur_end > cur_begin) {
-            ph.tile_info.insert(ph.tile_info.end(),
-                                {(int32_t)cur_begin, (int32_t)cur_end, -1, cur_sync ? 1 : 0});
-            ph.any_sync |= cur_sync;
+    auto emit = [&](const std::vector<int64_t>& its, bool sync, int hid, int q) {
+        for (int k = 0; k < W; k++) {
+            if (k < (int)its.size()) {
+                ph.slot_item.push_back((int32_t)its[k]);
+                ph.slot_aux.push_back(lc[its[k]] | (1 << 16) | (sync ? 1 << 17 : 0) |
+                                      (hid >= 0 ? 1 << 18 : 0));
+            } else {
+                ph.slot_item.push_back(-1);
+                ph.slot_aux.push_back(sync ? 1 << 17 : 0);
+            }
         }
-        cur_begin = cur_end;
+        ph.tile_heavy.push_back(hid);
+        ph.tile_heavy.push_back(q);
+        ph.any_sync |= sync;
+    };
+    auto close = [&]() {
+        if (!cur.empty()) emit(cur, cur_sync, -1, 0);
+        cur.clear();
         cur_sync = false;
     };
     int64_t i = 0;
     for (int64_t P = 0; P < nP; P++) {
-        int64_t a = i;
+        const int64_t a = i;
         while (i < NI && ph.item_panel[i] == P) i++;
         const int64_t n = i - a;
         if (n > 1) ph.n_split_items += (int32_t)n;
@@ -273,38 +286,48 @@ void build_tiles(PlanHost& ph, int W) {
                                  {(int32_t)P, ph.n_heavy_tiles, (int32_t)nt, 0});
             for (int64_t q = 0; q < nt; q++) {
                 const int64_t b0 = a + (q * n) / nt, b1 = a + ((q + 1) * n) / nt;
-                for (int64_t j = b0; j < b1; j++)
-                    ph.item_aux[j] = 0 | ((int32_t)(b1 - b0) << 8);
-                ph.tile_info.insert(ph.tile_info.end(),
-                                    {(int32_t)b0, (int32_t)b1, hid, (int32_t)(1 | (q << 1))});
+                std::vector<int64_t> its;
+                for (int64_t j = b0; j < b1; j++) {
+                    lc[j] = 0 | ((int32_t)(b1 - b0) << 8);
+                    its.push_back(j);
+                }
+                emit(its, true, hid, (int)q);
             }
             ph.n_heavy_tiles += (int32_t)nt;
-            ph.any_sync = true;
-            cur_begin = cur_end = i;
             continue;
         }
-        if (cur_end - cur_begin + n > W) close();
-        const int32_t lead = (int32_t)(a - cur_begin);
-        for (int64_t j = a; j < i; j++) ph.item_aux[j] = lead | ((int32_t)n << 8);
+        if ((int64_t)cur.size() + n > W) close();
+        const int32_t lead = (int32_t)cur.size();
+        for (int64_t j = a; j < i; j++) {
+            lc[j] = lead | ((int32_t)n << 8);
+            cur.push_back(j);
+        }
         if (n > 1) cur_sync = true;
-        cur_end = i;
     }
     close();
-    ph.n_tiles = (int)(ph.tile_info.size() / 4);
+    ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
     Params p;
     p.h = 4;
     p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
-    p.ufk = 4;
-    // expected gcols for a uniform pattern at h=4; item size so
-    // that about 64 warps per SM are available, clamped.
+    // Expected stream length per panel and gcol count for a uniform pattern
+    // (SURVEY App. A).  Item size: at least 16 columns, about one wave of 32
+    // resident warps per SM, and typical panels split into <= 16 items so that
+    // they combine inside one CTA tile.
     const double d = (double)nnz / ((double)m * (double)k);
     const double s = 1.0 - d;
-    const double G = std::ceil((double)m / p.h) * (double)k * (1.0 - std::pow(s, p.h));
-    const double target_items = (double)n_sm * 64.0;
-    int64_t T = (int64_t)std::ceil(G / target_items);
+    // UFi by sparsity (§3.5): enumeration pays when the expected
+    // pattern popcount p = h(1-s)/(1-s^h) is well above 1; the predicated
+    // pattern rows cost h FMA slots per column.
+    p.h = s >= 0.94 ? 1 : s >= 0.85 ? 2 : 4;
+    // UFk: B rows in flight per warp, bounded by registers (U*bCols/32 floats)
+    p.ufk = (bcols <= 64 || (bcols <= 128 && p.h <= 2)) ? 8 : 4;
+    const double sp = (double)k * (1.0 - std::pow(s, p.h));
+    const double G = std::ceil((double)m / p.h) * sp;
+    int64_t T = (int64_t)std::ceil(G / ((double)n_sm * 32.0));
+    T = std::max<int64_t>(T, (int64_t)std::ceil(sp / 16.0));
     T = std::max<int64_t>(T, 16);
     T = std::min<int64_t>(T, 1 << 20);
     p.T = (int)T;

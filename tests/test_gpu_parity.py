@@ -120,8 +120,6 @@ def test_bcols_tails_scalar_and_vector(torch_cuda, n):
     A, B = synth.dyadic_twin(A0, n, n + 1)
     C, _ = run_escs(torch_cuda, A, B)
     check_exact(A, B, C)
-    A0.vals[:] = synth.random_csr(203, 150, 3000, n, empty_rows=(0, 5, 6, 7, 8),
-                                  dense_rows=(100,)).vals
     B = synth.dense_b(150, n, 3)
     C, _ = run_escs(torch_cuda, A0, B)
     check_tol(A0, B, C)
@@ -133,9 +131,7 @@ def test_parameter_sweep_exact(torch_cuda, ufi, variant):
     A0 = synth.random_csr(130, 257, 9000, ufi, empty_rows=(3, 64, 65, 66, 67), dense_rows=(9,))
     for n in (32, 64, 128):
         A, B = synth.dyadic_twin(A0, n, ufi * 10 + n)
-        for T, w, ufk in ((1, 1, 2), (3, 3, 4), (16, 8, 8), (1000, 16, 4), (7, 2, 2)):
-            if variant == 2 and ufk != 4:
-                continue
+        for T, w, ufk in ((1, 1, 8), (3, 3, 4), (16, 8, 8), (1000, 8, 4), (7, 2, 4)):
             C, _ = run_escs(torch_cuda, A, B, ufi=ufi, T=T, cta_warps=w, ufk=ufk, variant=variant)
             check_exact(A, B, C)
 
