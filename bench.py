@@ -265,7 +265,9 @@ def compare_baselines(torch, problems, dev, stream):
         t_cublas = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 0, sp), stream)
         t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
         del Ad
+        inf = d["plan"].info
         rows.append({"case": p.name, "escs_us": 1e3 * t_escs,
+                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "n_tiles", "n_heavy", "G")},
                      "cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
                      "cublas_us": 1e3 * t_cublas, "cublas_tf32_us": 1e3 * t_tf32,
                      "gflops_escs": p.flops / (t_escs * 1e-3) / 1e9})

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -42,6 +43,13 @@ int sm_count_of_current_device() {
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
     return n > 0 ? n : 148;
+}
+
+bool env_sets(const char* key) {
+    const char* e = std::getenv("ESCS_PARAMS");
+    if (!e) return false;
+    std::string s = std::string(",") + e, k = std::string(",") + key + "=";
+    return s.find(k) != std::string::npos;
 }
 
 // ESCS_PARAMS="ufi=4,T=64,warps=8,variant=1,ufk=4"

@@ -116,31 +116,79 @@ struct ScalarMap {
     }
 };
 
-// Stage the values of one 32-column chunk: lane l holds, for its column, the
-// value of every pattern row r in w[r] (0 for rows outside the pattern),
-// read through the slot map.  Slots of a panel's stream are contiguous in
-// stream order with popcount(mask) slots per column, pattern rows ascending
-// (Reading R1), so the lane's first slot is the chunk base plus an exclusive
-// warp scan of the popcounts.
+// Per-warp staging area in shared memory, double-buffered by chunk: the 32
+// packed words of a chunk and, per column, the value of every pattern row
+// (0 for rows outside the pattern), so one broadcast LDS gives a column's
+// pattern and all its row values.
 template <int H>
-__device__ __forceinline__ int stage_values(const KParams& p, int pk, int sbase, float (&w)[H],
-                                            int lane) {
+struct Stage {
+    static constexpr int HP = H == 3 ? 4 : H;   // row values padded to a vector
+    int pk[2][32];
+    float w[2][32][HP];
+};
+
+// Load chunk `c` of the item into registers (packed word + row values of
+// this lane's column).  Slots of a panel's stream are contiguous in stream
+// order, popcount(mask) per column, pattern rows ascending (Reading R1), so
+// the lane's first slot is the chunk base plus an exclusive warp scan of the
+// popcounts.  Returns the slot base of the next chunk.
+template <int H, bool PROBE>
+__device__ __forceinline__ int fetch_chunk(const KParams& p, const int* gp, int n, int c0,
+                                           int sbase, int lane, int& pk, float (&w)[H]) {
+    pk = (c0 + lane < n) ? ld_stream(gp + c0 + lane) : 0;
     const unsigned mask = (unsigned)pk >> kColBits;
-    const unsigned lt = (1u << lane) - 1u;
-    int excl = 0, total = 0;
+    if constexpr (PROBE) {
 #pragma unroll
-    for (int bit = 0; bit < 3; bit++) {
-        const unsigned bal = __ballot_sync(kFull, (__popc(mask) >> bit) & 1);
-        excl += __popc(bal & lt) << bit;
-        total += __popc(bal) << bit;
-    }
-    const int* sp = p.slot + sbase + excl;
+        for (int r = 0; r < H; r++) w[r] = 0.f;
+        return sbase;
+    } else {
+        const unsigned lt = (1u << lane) - 1u;
+        int excl = 0, total = 0;
 #pragma unroll
-    for (int r = 0; r < H; r++) {
-        const int rank = __popc(mask & ((1u << r) - 1u));
-        w[r] = ((mask >> r) & 1u) ? __ldg(p.vals + ld_stream(sp + rank)) : 0.f;
+        for (int bit = 0; bit < 3; bit++) {
+            const unsigned bal = __ballot_sync(kFull, (__popc(mask) >> bit) & 1);
+            excl += __popc(bal & lt) << bit;
+            total += __popc(bal) << bit;
+        }
+        const int* sp = p.slot + sbase + excl;
+#pragma unroll
+        for (int r = 0; r < H; r++) {
+            const int rank = __popc(mask & ((1u << r) - 1u));
+            w[r] = ((mask >> r) & 1u) ? __ldg(p.vals + ld_stream(sp + rank)) : 0.f;
+        }
+        return sbase + total;
     }
-    return sbase + total;
+}
+
+template <int H>
+__device__ __forceinline__ void put_chunk(Stage<H>& st, int buf, int lane, int pk,
+                                          const float (&w)[H]) {
+    st.pk[buf][lane] = pk;
+    if constexpr (Stage<H>::HP == 4) {
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int r = 0; r < H; r++) x[r] = w[r];
+        *reinterpret_cast<float4*>(&st.w[buf][lane][0]) = make_float4(x[0], x[1], x[2], x[3]);
+    } else if constexpr (H == 2) {
+        *reinterpret_cast<float2*>(&st.w[buf][lane][0]) = make_float2(w[0], w[1]);
+    } else {
+        st.w[buf][lane][0] = w[0];
+    }
+}
+
+template <int H>
+__device__ __forceinline__ void get_vals(const Stage<H>& st, int buf, int s, float (&a)[H]) {
+    if constexpr (Stage<H>::HP == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(&st.w[buf][s][0]);
+        const float y[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int r = 0; r < H; r++) a[r] = y[r];
+    } else if constexpr (H == 2) {
+        const float2 x = *reinterpret_cast<const float2*>(&st.w[buf][s][0]);
+        a[0] = x.x; a[1] = x.y;
+    } else {
+        a[0] = st.w[buf][s][0];
+    }
 }
 
 // Walk one item: columns [beg, end) of the gcol stream, values from sbase.
@@ -149,31 +197,25 @@ __device__ __forceinline__ int stage_values(const KParams& p, int pk, int sbase,
 // pattern accumulate a*b -- the enumerated block of Listing 4,
 // realised as warp-uniform predicates on the pattern bits (the pattern is the
 // same for all lanes), so structural zeros are never multiplied and the code
-// stays one compact body for all 2^UFi - 1 patterns.
+// stays one compact body for all 2^UFi - 1 patterns.  The next chunk's
+// columns and values are fetched while the current chunk computes.
 template <int H, class Map, int U, bool PROBE>
-__device__ __forceinline__ void walk(const KParams& p, int beg, int end, int sbase,
+__device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, int end, int sbase,
                                      float (&acc)[H][Map::F], int lane) {
     constexpr int F = Map::F;
     static_assert(32 % U == 0, "UFK must divide 32");
     const int n = end - beg;
     const int* gp = p.gpk + beg;
-    int pk0 = (lane < n) ? ld_stream(gp + lane) : 0;
-    int pk1 = (32 + lane < n) ? ld_stream(gp + 32 + lane) : 0;
-    float v0[H], v1[H];
-    if constexpr (!PROBE) {
-        sbase = stage_values<H>(p, pk0, sbase, v0, lane);
-    } else {
-#pragma unroll
-        for (int j = 0; j < H; j++) v0[j] = 0.f;
-    }
+    int pk;
+    float w[H];
+    sbase = fetch_chunk<H, PROBE>(p, gp, n, 0, sbase, lane, pk, w);
+    put_chunk<H>(st, 0, lane, pk, w);
+    __syncwarp();
+    int buf = 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < n; c0 += 32) {
-        // one chunk ahead: packed words of chunk+1 are in pk1; stage its values
-        int pk2 = 0;
-        if (c0 + 32 < n) {
-            pk2 = (c0 + 64 + lane < n) ? ld_stream(gp + c0 + 64 + lane) : 0;
-            if constexpr (!PROBE) sbase = stage_values<H>(p, pk1, sbase, v1, lane);
-        }
+        const bool more = c0 + 32 < n;
+        if (more) sbase = fetch_chunk<H, PROBE>(p, gp, n, c0 + 32, sbase, lane, pk, w);
         const int cn = min(32, n - c0);
         // columns past the item end have pk = 0: row 0 is loaded, pattern 0
         // predicates every FMA off
@@ -183,7 +225,7 @@ __device__ __forceinline__ void walk(const KParams& p, int beg, int end, int sba
             int pq[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                pq[u] = __shfl_sync(kFull, pk0, s + u);
+                pq[u] = st.pk[buf][s + u];
                 Map::load(b[u], p.B + (size_t)(pq[u] & kColMask) * p.n, p.n, lane);
             }
 #pragma unroll
@@ -194,21 +236,23 @@ __device__ __forceinline__ void walk(const KParams& p, int beg, int end, int sba
                     for (int f = 0; f < F; f++)
                         if (mk) acc[0][f] += b[u][f];
                 } else {
+                    float a[H];
+                    get_vals<H>(st, buf, s + u, a);
 #pragma unroll
                     for (int row = 0; row < H; row++) {
-                        const float a = __shfl_sync(kFull, v0[row], s + u);
                         const bool on = (mk >> row) & 1u;
 #pragma unroll
                         for (int f = 0; f < F; f++)
-                            if (on) acc[row][f] = fmaf(a, b[u][f], acc[row][f]);
+                            if (on) acc[row][f] = fmaf(a[row], b[u][f], acc[row][f]);
                     }
                 }
             }
         }
-        pk0 = pk1;
-        pk1 = pk2;
-#pragma unroll
-        for (int j = 0; j < H; j++) v0[j] = v1[j];
+        if (more) {
+            put_chunk<H>(st, buf ^ 1, lane, pk, w);
+            __syncwarp();
+            buf ^= 1;
+        }
     }
 }
 
@@ -222,15 +266,23 @@ __device__ __forceinline__ void store_rows(const KParams& p, int panel, const fl
     }
 }
 
+template <int H, class Map>
+__host__ __device__ constexpr int warp_smem_floats() {
+    return (int)(sizeof(Stage<H>) / 4) > H * 32 * Map::F ? (int)(sizeof(Stage<H>) / 4)
+                                                           : H * 32 * Map::F;
+}
+
 // Item slots are tile-major: CTA b owns slots [b*W, b*W + W), W = warps per
 // CTA; slot aux = lead | cnt << 8 | active << 16 | tile_sync << 17 |
 // tile_heavy << 18 (lead: warp of the panel's first item in this tile, cnt:
 // the panel's items in this tile).
 template <int H, class Map, int U, bool PROBE>
-__global__ void __launch_bounds__(512, 2) esc_spmm_kernel(KParams p) {
-    extern __shared__ __align__(16) float smem[];   // [W][H][32F] partials of split panels
+__global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
+    // per warp: the chunk staging area during the walk, then (aliased) the
+    // warp's partial tile [H][32F] for the combine of split panels
+    extern __shared__ __align__(16) float smem[];
     constexpr int F = Map::F;
-    constexpr int WS = H * 32 * F;
+    constexpr int WS = warp_smem_floats<H, Map>();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int slot = blockIdx.x * (blockDim.x >> 5) + w;
     const int aux = p.item_aux[slot];
@@ -246,7 +298,9 @@ __global__ void __launch_bounds__(512, 2) esc_spmm_kernel(KParams p) {
     if (active) {
         const int4 it = p.items[slot];
         panel = it.x;
-        walk<H, Map, U, PROBE>(p, it.y, it.z, it.w, acc, lane);
+        walk<H, Map, U, PROBE>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y, it.z,
+                               it.w, acc, lane);
+        __syncwarp();   // staging reads done before the area holds the partial
     }
 
     if constexpr (PROBE) {

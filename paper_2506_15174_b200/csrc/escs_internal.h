@@ -72,5 +72,7 @@ int prepare_kernels(const DevPlan& dp);
 // Does a kernel instance exist for this configuration?
 bool kernel_supported(int h, int bcols, int variant, int ufk);
 size_t smem_bytes(const DevPlan& dp);
+// Resident CTAs per SM for this plan's launch configuration.
+int blocks_per_sm(const DevPlan& dp);
 
 }  // namespace escs

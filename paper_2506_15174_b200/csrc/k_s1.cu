@@ -4,12 +4,16 @@ namespace escs {
 namespace kern {
 KernelFn get_s1(int h, int ufk, bool probe) {
     using M = ScalarMap<1>;
+    if (h == 1 && ufk == 2 && !probe) return esc_spmm_kernel<1, M, 2, false>;
     if (h == 1 && ufk == 4 && !probe) return esc_spmm_kernel<1, M, 4, false>;
     if (h == 1 && ufk == 8 && !probe) return esc_spmm_kernel<1, M, 8, false>;
+    if (h == 2 && ufk == 2 && !probe) return esc_spmm_kernel<2, M, 2, false>;
     if (h == 2 && ufk == 4 && !probe) return esc_spmm_kernel<2, M, 4, false>;
     if (h == 2 && ufk == 8 && !probe) return esc_spmm_kernel<2, M, 8, false>;
+    if (h == 3 && ufk == 2 && !probe) return esc_spmm_kernel<3, M, 2, false>;
     if (h == 3 && ufk == 4 && !probe) return esc_spmm_kernel<3, M, 4, false>;
     if (h == 3 && ufk == 8 && !probe) return esc_spmm_kernel<3, M, 8, false>;
+    if (h == 4 && ufk == 2 && !probe) return esc_spmm_kernel<4, M, 2, false>;
     if (h == 4 && ufk == 4 && !probe) return esc_spmm_kernel<4, M, 4, false>;
     if (h == 4 && ufk == 8 && !probe) return esc_spmm_kernel<4, M, 8, false>;
     return nullptr;

@@ -70,8 +70,10 @@ static int lane_floats(int n, bool vec) {
 
 static size_t smem_for(const DevPlan& dp, bool vec) {
     const int F = lane_floats(dp.bcols, vec);
-    if (!dp.any_sync) return 0;
-    return (size_t)dp.cta_warps * dp.h * 32 * F * sizeof(float);
+    const int hp = dp.h == 3 ? 4 : dp.h;
+    const size_t stage = (size_t)2 * 32 * (1 + hp);           // Stage<H> floats
+    const size_t part = (size_t)dp.h * 32 * F;   // kernel strides warps by max(stage, part)
+    return (size_t)dp.cta_warps * (stage > part ? stage : part) * sizeof(float);
 }
 
 size_t smem_bytes(const DevPlan& dp) { return smem_for(dp, dp.variant == 1); }
@@ -99,6 +101,19 @@ int prepare_kernels(const DevPlan& dp) {
         }
     }
     return 0;
+}
+
+int blocks_per_sm(const DevPlan& dp) {
+    const bool vec = dp.variant == 1;
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
+    if (!fn) return 1;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, 32 * dp.cta_warps,
+                                                      smem_for(dp, vec)) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    return nb > 0 ? nb : 1;
 }
 
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,

@@ -308,27 +308,33 @@ void build_tiles(PlanHost& ph, int W) {
     ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 
+// Parameter table (§3.5 Scheduler & Tuner): fitted to the
+// profiling sweep of tools/tune.py on B200 (profiles/tune_*.json).
+//  * UFi: the enumerated blocks pay (fewer gathered B rows, p = h(1-s)/(1-s^h))
+//    only at low sparsity with narrow B rows and a small, cache-resident B;
+//    otherwise the predicated pattern rows cost more than they save -> 1.
+//  * UFk: B rows in flight per warp, bounded by registers (UFk * bCols/32).
+//  * T: about 3200 items per launch (one wave of ~22 warps per SM on 148
+//    SMs, each item long enough to amortise its ~4 dependent round trips),
+//    at least 16 columns (8 for tiny problems), rounded so that a typical
+//    panel splits into equal items.
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
     Params p;
-    p.h = 4;
-    p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
-    // Expected stream length per panel and gcol count for a uniform pattern
-    // (SURVEY App. A).  Item size: at least 16 columns, about one wave of 32
-    // resident warps per SM, and typical panels split into <= 16 items so that
-    // they combine inside one CTA tile.
     const double d = (double)nnz / ((double)m * (double)k);
     const double s = 1.0 - d;
-    // UFi by sparsity (§3.5): enumeration pays when the expected
-    // pattern popcount p = h(1-s)/(1-s^h) is well above 1; the predicated
-    // pattern rows cost h FMA slots per column.
-    p.h = s >= 0.94 ? 1 : s >= 0.85 ? 2 : 4;
-    // UFk: B rows in flight per warp, bounded by registers (U*bCols/32 floats)
-    p.ufk = (bcols <= 64 || (bcols <= 128 && p.h <= 2)) ? 8 : 4;
-    const double sp = (double)k * (1.0 - std::pow(s, p.h));
+    p.h = (s <= 0.75 && bcols <= 64 && k <= 1024) ? 4 : 1;
+    p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
+    p.ufk = bcols <= 64 ? 8 : 4;
+    const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
-    int64_t T = (int64_t)std::ceil(G / ((double)n_sm * 32.0));
-    T = std::max<int64_t>(T, (int64_t)std::ceil(sp / 16.0));
-    T = std::max<int64_t>(T, 16);
+    const double target_items = 3200.0 * (double)n_sm / 148.0;
+    int64_t T = (int64_t)std::ceil(G / target_items);
+    const int64_t Tmin = G < 16.0 * 4.0 * n_sm ? 8 : 16;
+    T = std::max<int64_t>(T, Tmin);
+    if (sp >= 1.0) {
+        const int64_t per = std::max<int64_t>(1, (int64_t)std::ceil(sp / (double)T));
+        T = std::max<int64_t>(Tmin, (int64_t)std::ceil(sp / (double)per));
+    }
     T = std::min<int64_t>(T, 1 << 20);
     p.T = (int)T;
     p.cta_warps = 0;   // auto from the item distribution
