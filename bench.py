@@ -54,6 +54,18 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
 
 
+def committed_traffic(workload_name):
+    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        if t.get("workload") == workload_name:
+            return t["dram_bytes_per_launch"], t["source"]
+    except Exception:
+        pass
+    return None, None
+
+
 def workload(name):
     from paper_2506_15174_b200 import synth
     if name == "transformer":
@@ -292,14 +304,12 @@ def run_escs(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and "WORLD_SIZE" in os.environ:
-        pass
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
 
-    from paper_2506_15174_b200 import escs, synth
+    from paper_2506_15174_b200 import escs, shard
 
     problems, desc = workload(args.workload)
     # row-block shard of every problem; world = 1 -> whole problem
@@ -308,10 +318,8 @@ def run_escs(args):
     plan_s = 0.0
     plan_info = []
     for p in problems:
-        r0, r1 = synth.shard_bounds(p.A.m, world, rank)
-        A = synth.row_block(p.A, r0, r1) if world > 1 else p.A
         t0 = time.perf_counter()
-        pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols)
+        A, pl = shard.plan_shard(p.A, p.bcols, world, rank)
         plan_s += time.perf_counter() - t0
         info = pl.info
         plan_info.append(info)
@@ -369,6 +377,21 @@ def run_escs(args):
             torch.cuda._sleep(sleep_cycles)
             step(pl_ev[s])
         barrier()
+    # ---- gather probe: same walk and B-row loads, no values/FMAs (t_probe)
+    probe_ms = None
+    if all(d["plan"].info["variant"] == 1 for _, d in shard_problems):
+        sinks = [torch.empty(d["plan"].info["n_tiles"] * 32 * d["plan"].info["cta_warps"],
+                             device=device) for _, d in shard_problems]
+        pr_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
+        for s_ in range(args.steps):
+            flush.zero_()
+            torch.cuda._sleep(sleep_cycles)
+            for i, (p, d) in enumerate(shard_problems):
+                pr_ev[s_][i][0].record(stream)
+                escs.escs_gather_probe(d["plan"], d["B"], sinks[i], stream)
+                pr_ev[s_][i][1].record(stream)
+        barrier()
+        probe_ms = float(sum(a.elapsed_time(b) for row in pr_ev for a, b in row))
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
     kern_ms = np.array([[a.elapsed_time(b) for a, b in pl_ev[s]] for s in range(args.steps)])
@@ -403,16 +426,23 @@ def run_escs(args):
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
 
+    # ---- optional all-gather of C (NCCL), timed separately (not on the hot path)
+    allgather_ms = None
+    if world > 1 and args.allgather:
+        ga, gb = ev(), ev()
+        barrier()
+        ga.record(stream)
+        for p, d in shard_problems:
+            shard.all_gather_rows(d["C"], p.A.m, world)
+        gb.record(stream)
+        barrier()
+        allgather_ms = shard.max_over_ranks([ga.elapsed_time(gb)], device)[0]
+
     # ---- reduce over ranks: flops SUM, times MAX
     my_flops = sum(d["flops"] for _, d in shard_problems)
     my_bytes = sum(d["bytes"] for _, d in shard_problems)
-    vec = torch.tensor([total_ms, e2e_ms, kern_ms_sum], dtype=torch.float64, device=device)
-    sums = torch.tensor([my_flops, my_bytes], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-    total_ms, e2e_ms, kern_ms_sum = (float(x) for x in vec.tolist())
-    flops_all, bytes_all = (float(x) for x in sums.tolist())
+    total_ms, e2e_ms, kern_ms_sum = shard.max_over_ranks([total_ms, e2e_ms, kern_ms_sum], device)
+    flops_all, bytes_all = shard.sum_over_ranks([my_flops, my_bytes], device)
 
     result = None
     if rank == 0:
@@ -425,6 +455,7 @@ def run_escs(args):
         per_prob = kern_ms.mean(axis=0)
         dom = int(np.argmax(per_prob))
         clocks = clk.summary()
+        traffic, traffic_src = committed_traffic(args.workload) if world == 1 else (None, None)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
@@ -433,19 +464,27 @@ def run_escs(args):
                        "l2": "flushed before every step (256 MiB write); each problem touched once per step",
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "variant")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": my_bytes / nprob,
                          "peak_source": peak_src,
                          "algorithmic_bytes": "8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols per launch (CSR A, B, C once; SURVEY 8(d))",
                          "kernel": "escs_spmm (esc_spmm_kernel), all launches of the step",
                          "kernel_ms_per_step": float(kern_ms.sum() / K),
                          "gather_GBps": gather,
-                         "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)"},
+                         "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)",
+                         "attainable": None if probe_ms is None else {
+                             "probe_ms_per_step": probe_ms / K,
+                             "frac": probe_ms / float(kern_ms.sum()),
+                             "what": "t_probe / t_kernel: escs_gather_probe runs the same item walk and B-row gathers without values or FMAs (measured gather ceiling of this plan)"}},
             "gpu_launches": nprob * K,
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "plan_seconds": plan_s,
         }
+        if allgather_ms is not None:
+            result["allgather_ms_per_step"] = allgather_ms
         if world == 1 and not args.no_cpu:
             v, reps, secs, thr = oracle_time(problems, budget_s=args.cpu_budget)
             result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
@@ -475,6 +514,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--cases-out", default=None)
+    ap.add_argument("--allgather", action="store_true",
+                    help="N>1: also time the optional NCCL all-gather of C (not on the hot path)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

@@ -43,7 +43,7 @@ struct KParams {
     const int2* __restrict__ tile_heavy; // per tile: heavy id, ordinal (heavy tiles only)
     const int4* __restrict__ heavy;    // panel, ws_base, ntiles, 0
     float* ws;
-    int* counters;
+    int* counters;                     // heavy-panel arrival counters
     const float* __restrict__ vals;
     const float* __restrict__ B;
     float* __restrict__ C;
@@ -191,6 +191,76 @@ __device__ __forceinline__ void get_vals(const Stage<H>& st, int buf, int s, flo
     }
 }
 
+// UFi = 1: every column has the single pattern 0b1 and the slot map is the
+// identity (a panel is one CSR row, its value slots are that row's CSR
+// positions in order), so column i of an item reads vals[sbase + i]
+// directly -- contiguous, no second indirection.  Column index and value of
+// the current and next chunk live in registers and are broadcast with
+// __shfl_sync.  Full batches run unpredicated; the last partial batch of an
+// item predicates its FMAs (structural zeros are never multiplied).
+template <class Map, int U, bool PROBE>
+__device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sbase,
+                                      float (&acc)[1][Map::F], int lane) {
+    constexpr int F = Map::F;
+    const int n = end - beg;
+    const int* gp = p.gpk + beg;
+    const float* vp = p.vals + sbase;
+    int pk0 = 0, pk1 = 0;
+    float v0 = 0.f, v1 = 0.f;
+    if (lane < n) {
+        pk0 = ld_stream(gp + lane);
+        if constexpr (!PROBE) v0 = __ldg(vp + lane);
+    }
+    if (32 + lane < n) {
+        pk1 = ld_stream(gp + 32 + lane);
+        if constexpr (!PROBE) v1 = __ldg(vp + 32 + lane);
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        int pk2 = 0;
+        float v2 = 0.f;
+        if (c0 + 64 + lane < n) {
+            pk2 = ld_stream(gp + c0 + 64 + lane);
+            if constexpr (!PROBE) v2 = __ldg(vp + c0 + 64 + lane);
+        }
+        const int cn = min(32, n - c0);
+        int s = 0;
+#pragma unroll 1
+        for (; s + U <= cn; s += U) {
+            float b[U][F];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int c = __shfl_sync(kFull, pk0, s + u) & kColMask;
+                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lane);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, s + u);
+#pragma unroll
+                for (int f = 0; f < F; f++) acc[0][f] = fmaf(a, b[u][f], acc[0][f]);
+            }
+        }
+        if (s < cn) {   // partial batch
+            float b[U][F];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int c = __shfl_sync(kFull, pk0, (s + u) & 31) & kColMask;
+                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lane);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, (s + u) & 31);
+                const bool ok = s + u < cn;
+#pragma unroll
+                for (int f = 0; f < F; f++)
+                    if (ok) acc[0][f] = fmaf(a, b[u][f], acc[0][f]);
+            }
+        }
+        pk0 = pk1; v0 = v1;
+        pk1 = pk2; v1 = v2;
+    }
+}
+
 // Walk one item: columns [beg, end) of the gcol stream, values from sbase.
 // Columns are processed in batches of U: U gathered B rows in flight (thread
 // coarsening over k, "UFk"), then for every column the rows of its
@@ -272,20 +342,20 @@ __host__ __device__ constexpr int warp_smem_floats() {
                                                            : H * 32 * Map::F;
 }
 
-// Item slots are tile-major: CTA b owns slots [b*W, b*W + W), W = warps per
-// CTA; slot aux = lead | cnt << 8 | active << 16 | tile_sync << 17 |
-// tile_heavy << 18 (lead: warp of the panel's first item in this tile, cnt:
-// the panel's items in this tile).
+// One CTA tile.  Item slots are tile-major: tile t owns slots [t*W, t*W + W),
+// W = warps per CTA; slot aux = lead | cnt << 8 | active << 16 | tile_sync << 17
+// | tile_heavy << 18 (lead: warp of the panel's first item in this tile, cnt:
+// the panel's items in this tile).  Every warp of the CTA calls this; the
+// __syncthreads below is reached by all of them when the tile needs a combine
+// (the flag is tile-uniform).
 template <int H, class Map, int U, bool PROBE>
-__global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
-    // per warp: the chunk staging area during the walk, then (aliased) the
-    // warp's partial tile [H][32F] for the combine of split panels
-    extern __shared__ __align__(16) float smem[];
+__device__ __forceinline__ void process_tile(const KParams& p, float* smem, int tile, int w,
+                                             int lane) {
     constexpr int F = Map::F;
     constexpr int WS = warp_smem_floats<H, Map>();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int slot = blockIdx.x * (blockDim.x >> 5) + w;
+    const int slot = tile * (blockDim.x >> 5) + w;
     const int aux = p.item_aux[slot];
+    const int4 it = p.items[slot];   // independent of aux: both loads in flight together
     const bool active = (aux >> 16) & 1;
 
     float acc[H][F];
@@ -294,21 +364,23 @@ __global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
 #pragma unroll
         for (int f = 0; f < F; f++) acc[r][f] = 0.f;
 
-    int panel = 0;
+    const int panel = it.x;
     if (active) {
-        const int4 it = p.items[slot];
-        panel = it.x;
-        walk<H, Map, U, PROBE>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y, it.z,
-                               it.w, acc, lane);
-        __syncwarp();   // staging reads done before the area holds the partial
+        if constexpr (H == 1) {
+            walk1<Map, U, PROBE>(p, it.y, it.z, it.w, acc, lane);
+        } else {
+            walk<H, Map, U, PROBE>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y,
+                                   it.z, it.w, acc, lane);
+        }
     }
+    __syncwarp();   // staging reads done before the area holds the partial
 
     if constexpr (PROBE) {
         if (active) {
             float s = 0.f;
 #pragma unroll
             for (int f = 0; f < F; f++) s += acc[0][f];
-            p.C[((size_t)blockIdx.x * blockDim.x) + threadIdx.x] = s;
+            p.C[(size_t)slot * 32 + lane] += s;
         }
         return;
     } else {
@@ -357,8 +429,8 @@ __global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
             return;
         }
         // heavy panel: its tiles combine through the global workspace
-        const int2 th = p.tile_heavy[blockIdx.x];      // heavy id, ordinal
-        const int4 hv = p.heavy[th.x];                  // panel, ws_base, ntiles
+        const int2 th = p.tile_heavy[tile];      // heavy id, ordinal
+        const int4 hv = p.heavy[th.x];           // panel, ws_base, ntiles
         float* wsq = p.ws + (size_t)(hv.y + th.y) * H * n;
 #pragma unroll
         for (int r = 0; r < H; r++)
@@ -392,6 +464,16 @@ __global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
         store_rows<H, Map>(p, hv.x, acc, lane);
         if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
     }
+}
+
+// One CTA per tile.  (A persistent variant with a dynamic tile counter was
+// measured and dropped: the hardware block scheduler already dispatches CTAs
+// dynamically, and the counter atomics and extra barriers cost 0.2-1.5 us per
+// launch on the latency-bound suite -- profiles/r1_notes.md.)
+template <int H, class Map, int U, bool PROBE>
+__global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
+    extern __shared__ __align__(16) float smem[];
+    process_tile<H, Map, U, PROBE>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31);
 }
 
 using KernelFn = void (*)(KParams);

@@ -68,11 +68,11 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
 // Launch the gather probe (same walk, loads only).
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok);
 // Prepare kernel attributes (dynamic smem limits) once per plan.
-int prepare_kernels(const DevPlan& dp);
+int prepare_kernels(DevPlan& dp);
 // Does a kernel instance exist for this configuration?
 bool kernel_supported(int h, int bcols, int variant, int ufk);
 size_t smem_bytes(const DevPlan& dp);
 // Resident CTAs per SM for this plan's launch configuration.
-int blocks_per_sm(const DevPlan& dp);
+int blocks_per_sm(const DevPlan& dp, bool vec, bool probe);
 
 }  // namespace escs

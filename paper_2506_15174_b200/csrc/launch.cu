@@ -1,6 +1,8 @@
 // launch.cu -- kernel selection and the single launch behind escs_spmm.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "esc_kernel.cuh"
 #include "escs_internal.h"
 
@@ -78,7 +80,7 @@ static size_t smem_for(const DevPlan& dp, bool vec) {
 
 size_t smem_bytes(const DevPlan& dp) { return smem_for(dp, dp.variant == 1); }
 
-int prepare_kernels(const DevPlan& dp) {
+int prepare_kernels(DevPlan& dp) {
     // Kernel attributes are per function and shared by every plan: only ever
     // raise the dynamic shared memory limit (never lower it under another plan).
     for (int vec = 0; vec < 2; vec++) {
@@ -103,9 +105,8 @@ int prepare_kernels(const DevPlan& dp) {
     return 0;
 }
 
-int blocks_per_sm(const DevPlan& dp) {
-    const bool vec = dp.variant == 1;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
+int blocks_per_sm(const DevPlan& dp, bool vec, bool probe) {
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, probe);
     if (!fn) return 1;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, 32 * dp.cta_warps,

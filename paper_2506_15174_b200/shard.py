@@ -1,0 +1,67 @@
+"""Row-block sharding of A across ranks (north_star: "row-block
+sharding of A across the 8 GPUs of one box, with B replicated and no
+collective on the hot path except an optional NCCL all-gather of C").
+
+Rank r of G owns rows [r*m/G, (r+1)*m/G) of A and C; it plans its own shard
+(panels are shard-relative), B is replicated, and C blocks are independent.
+The optional all-gather of C uses torch.distributed (NCCL on GPUs, gloo in the
+CPU tests).  This module is plumbing only: no arithmetic of the method.
+"""
+from __future__ import annotations
+
+from . import synth
+
+
+def shard_rows(m: int, world: int, rank: int):
+    """Rows [r0, r1) owned by `rank`."""
+    return synth.shard_bounds(m, world, rank)
+
+
+def shard_matrix(A: "synth.CSR", world: int, rank: int) -> "synth.CSR":
+    r0, r1 = shard_rows(A.m, world, rank)
+    return synth.row_block(A, r0, r1) if world > 1 else A
+
+
+def plan_shard(A: "synth.CSR", bcols: int, world: int, rank: int, **params):
+    """escs plan of this rank's row block (host-only when params say so)."""
+    from . import escs
+    S = shard_matrix(A, world, rank)
+    if params:
+        return S, escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, bcols, **params)
+    return S, escs.escs_plan(S.m, S.k, S.nnz, S.rowptr, S.colidx, bcols)
+
+
+def all_gather_rows(C_local, m: int, world: int, group=None):
+    """Optional all-gather of the C row blocks into the full m x n C on every
+    rank.  Row blocks may differ by one row; they are padded to the largest
+    block for all_gather_into_tensor and trimmed afterwards."""
+    import torch
+    import torch.distributed as dist
+    n = C_local.shape[1]
+    blocks = [shard_rows(m, world, r) for r in range(world)]
+    rows_max = max(r1 - r0 for r0, r1 in blocks)
+    buf = torch.zeros((rows_max, n), dtype=C_local.dtype, device=C_local.device)
+    buf[:C_local.shape[0]] = C_local
+    out = torch.empty((world * rows_max, n), dtype=C_local.dtype, device=C_local.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * rows_max:r * rows_max + (r1 - r0)] for r, (r0, r1) in enumerate(blocks)]
+    return torch.cat(parts, 0)
+
+
+def max_over_ranks(values, device=None):
+    """Element-wise MAX over ranks (device-side times: the straggler decides)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def sum_over_ranks(values, device=None):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]

@@ -17,10 +17,20 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--config", default=None, help="c1/c4/c5 instead of a suite shape")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--case", default=None, help="a problem name from bench.py's workloads")
     a = ap.parse_args()
     import torch
     from paper_2506_15174_b200 import escs, synth
-    if a.config:
+    if a.case:
+        import bench
+        for wl in ("transformer", "resnet"):
+            hit = [q for q in bench.workload(wl)[0] if q.name == a.case]
+            if hit:
+                A, B = hit[0].A, hit[0].B
+                break
+        else:
+            raise SystemExit(f"no case {a.case}")
+    elif a.config:
         p = synth.config(a.config)
         A, B = p.A, p.B
     else:
