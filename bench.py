@@ -6,9 +6,11 @@
 
 A *step* is one pass of the whole hot path over the workload: one
 ``escs_spmm`` (one kernel launch) per problem of the workload with inputs
-resident in HBM.  Default workload (N=1): configs[1] of BASELINE.json, the
-sparse-Transformer suite {512x512, 2048x512, 512x2048} x {70,80,90,95,98}%
-x bCols {32,64,128} = 45 SpMMs per step.  With N>1 ranks (torchrun), every
+resident in HBM.  Default workload: the layer suite BASELINE.json's metric
+(geomean over "the sparse ResNet-50/Transformer layer suite at bCols
+32/64/128") is quoted on -- configs[1] Transformer {512x512, 2048x512,
+512x2048} + configs[2] ResNet-50 im2col {256x2304, 512x4608, 2048x512}, each
+at {70,80,90,95,98}% x bCols {32,64,128} = 90 SpMMs per step.  With N>1 ranks (torchrun), every
 problem is row-block sharded (rank r owns rows [r*m/N, (r+1)*m/N), B
 replicated, no collective on the hot path): total work is
 fixed, so scaling is "strong".
@@ -509,7 +511,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="escs", choices=["escs", "reference"])
-    ap.add_argument("--workload", default="transformer")
+    ap.add_argument("--workload", default="suite")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)

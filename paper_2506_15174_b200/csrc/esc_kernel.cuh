@@ -56,14 +56,17 @@ __device__ __forceinline__ int ld_stream(const int* p) {
     return r;
 }
 
-// Vector lane map: N = 32*F, lane owns columns [lane*F, lane*F + F).
-template <int F_>
+// Vector lane map: L lanes own one gathered B row of N = L*F floats (F
+// consecutive floats per lane, 128-bit loads for F >= 4), so a warp gathers
+// S = 32/L rows per step ("sub-warps"); sub-warp partial sums are reduced
+// with shfl_xor at the end of the item (the warp-level reduction of P:450).
+template <int L_, int F_>
 struct VecMap {
-    static constexpr int F = F_;
+    static constexpr int L = L_, F = F_, S = 32 / L_;
     static constexpr bool kVec = true;
-    __device__ static __forceinline__ int col(int lane, int f) { return lane * F + f; }
-    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lane) {
-        const float* q = row + lane * F;
+    __device__ static __forceinline__ int col(int lj, int f) { return lj * F + f; }
+    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lj) {
+        const float* q = row + lj * F;
         if constexpr (F == 1) {
             asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(b[0]) : "l"(q));
         } else if constexpr (F == 2) {
@@ -77,8 +80,8 @@ struct VecMap {
                              : "l"(q + 4 * v));
         }
     }
-    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lane) {
-        float* q = row + lane * F;
+    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lj) {
+        float* q = row + lj * F;
         if constexpr (F == 1) {
             q[0] = a[0];
         } else if constexpr (F == 2) {
@@ -94,23 +97,23 @@ struct VecMap {
 
 // Scalar lane map (the paper's map(j, 32*WarpTile), Listings 5-6): lane owns
 // columns lane + 32*f, f < WT, predicated on j < N.  Any N <= 32*WT, any
-// alignment.
+// alignment.  One gathered row per warp step.
 template <int WT>
 struct ScalarMap {
-    static constexpr int F = WT;
+    static constexpr int L = 32, F = WT, S = 1;
     static constexpr bool kVec = false;
-    __device__ static __forceinline__ int col(int lane, int f) { return lane + 32 * f; }
-    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int n, int lane) {
+    __device__ static __forceinline__ int col(int lj, int f) { return lj + 32 * f; }
+    __device__ static __forceinline__ void load(float (&b)[F], const float* row, int n, int lj) {
 #pragma unroll
         for (int f = 0; f < F; f++) {
-            const int j = lane + 32 * f;
+            const int j = lj + 32 * f;
             b[f] = (j < n) ? __ldg(row + j) : 0.f;
         }
     }
-    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int n, int lane) {
+    __device__ static __forceinline__ void store(float* row, const float (&a)[F], int n, int lj) {
 #pragma unroll
         for (int f = 0; f < F; f++) {
-            const int j = lane + 32 * f;
+            const int j = lj + 32 * f;
             if (j < n) row[j] = a[f];
         }
     }
@@ -196,12 +199,15 @@ __device__ __forceinline__ void get_vals(const Stage<H>& st, int buf, int s, flo
 // positions in order), so column i of an item reads vals[sbase + i]
 // directly -- contiguous, no second indirection.  Column index and value of
 // the current and next chunk live in registers and are broadcast with
-// __shfl_sync.  Full batches run unpredicated; the last partial batch of an
-// item predicates its FMAs (structural zeros are never multiplied).
+// __shfl_sync (each sub-warp reads its own column).  Full batches run
+// unpredicated; the last partial batch of an item predicates its FMAs
+// (structural zeros are never multiplied).
 template <class Map, int U, bool PROBE>
 __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sbase,
                                       float (&acc)[1][Map::F], int lane) {
-    constexpr int F = Map::F;
+    constexpr int F = Map::F, S = Map::S, US = U * S;
+    static_assert(32 % US == 0, "UFK * sub-warps must divide 32");
+    const int sub = lane / Map::L, lj = lane % Map::L;
     const int n = end - beg;
     const int* gp = p.gpk + beg;
     const float* vp = p.vals + sbase;
@@ -226,16 +232,16 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
         const int cn = min(32, n - c0);
         int s = 0;
 #pragma unroll 1
-        for (; s + U <= cn; s += U) {
+        for (; s + US <= cn; s += US) {
             float b[U][F];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int c = __shfl_sync(kFull, pk0, s + u) & kColMask;
-                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lane);
+                const int c = __shfl_sync(kFull, pk0, s + u * S + sub) & kColMask;
+                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lj);
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, s + u);
+                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, s + u * S + sub);
 #pragma unroll
                 for (int f = 0; f < F; f++) acc[0][f] = fmaf(a, b[u][f], acc[0][f]);
             }
@@ -244,13 +250,14 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
             float b[U][F];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const int c = __shfl_sync(kFull, pk0, (s + u) & 31) & kColMask;
-                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lane);
+                const int c = __shfl_sync(kFull, pk0, (s + u * S + sub) & 31) & kColMask;
+                Map::load(b[u], p.B + (size_t)c * p.n, p.n, lj);
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, (s + u) & 31);
-                const bool ok = s + u < cn;
+                const int ci = s + u * S + sub;
+                const float a = PROBE ? 1.f : __shfl_sync(kFull, v0, ci & 31);
+                const bool ok = ci < cn;
 #pragma unroll
                 for (int f = 0; f < F; f++)
                     if (ok) acc[0][f] = fmaf(a, b[u][f], acc[0][f]);
@@ -265,15 +272,16 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
 // Columns are processed in batches of U: U gathered B rows in flight (thread
 // coarsening over k, "UFk"), then for every column the rows of its
 // pattern accumulate a*b -- the enumerated block of Listing 4,
-// realised as warp-uniform predicates on the pattern bits (the pattern is the
-// same for all lanes), so structural zeros are never multiplied and the code
-// stays one compact body for all 2^UFi - 1 patterns.  The next chunk's
-// columns and values are fetched while the current chunk computes.
+// realised as predicates on the pattern bits (uniform within a sub-warp),
+// so structural zeros are never multiplied and the code stays one compact
+// body for all 2^UFi - 1 patterns.  The next chunk's columns and values are
+// fetched while the current chunk computes.
 template <int H, class Map, int U, bool PROBE>
 __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, int end, int sbase,
                                      float (&acc)[H][Map::F], int lane) {
-    constexpr int F = Map::F;
-    static_assert(32 % U == 0, "UFK must divide 32");
+    constexpr int F = Map::F, S = Map::S, US = U * S;
+    static_assert(32 % US == 0, "UFK * sub-warps must divide 32");
+    const int sub = lane / Map::L, lj = lane % Map::L;
     const int n = end - beg;
     const int* gp = p.gpk + beg;
     int pk;
@@ -290,13 +298,13 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
         // columns past the item end have pk = 0: row 0 is loaded, pattern 0
         // predicates every FMA off
 #pragma unroll 1
-        for (int s = 0; s < cn; s += U) {
+        for (int s = 0; s < cn; s += US) {
             float b[U][F];
             int pq[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                pq[u] = st.pk[buf][s + u];
-                Map::load(b[u], p.B + (size_t)(pq[u] & kColMask) * p.n, p.n, lane);
+                pq[u] = st.pk[buf][s + u * S + sub];
+                Map::load(b[u], p.B + (size_t)(pq[u] & kColMask) * p.n, p.n, lj);
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
@@ -307,7 +315,7 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
                         if (mk) acc[0][f] += b[u][f];
                 } else {
                     float a[H];
-                    get_vals<H>(st, buf, s + u, a);
+                    get_vals<H>(st, buf, s + u * S + sub, a);
 #pragma unroll
                     for (int row = 0; row < H; row++) {
                         const bool on = (mk >> row) & 1u;
@@ -326,20 +334,22 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
     }
 }
 
+// Row r of a panel tile is written by sub-warp r % S (after the sub-warp
+// reduction every sub-warp holds the totals).
 template <int H, class Map>
 __device__ __forceinline__ void store_rows(const KParams& p, int panel, const float (&a)[H][Map::F],
-                                           int lane) {
+                                           int sub, int lj) {
 #pragma unroll
     for (int r = 0; r < H; r++) {
         const int row = panel * H + r;
-        if (row < p.m) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lane);
+        if ((r % Map::S) == sub && row < p.m) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
     }
 }
 
 template <int H, class Map>
 __host__ __device__ constexpr int warp_smem_floats() {
-    return (int)(sizeof(Stage<H>) / 4) > H * 32 * Map::F ? (int)(sizeof(Stage<H>) / 4)
-                                                           : H * 32 * Map::F;
+    return (int)(sizeof(Stage<H>) / 4) > H * Map::L * Map::F ? (int)(sizeof(Stage<H>) / 4)
+                                                               : H * Map::L * Map::F;
 }
 
 // One CTA tile.  Item slots are tile-major: tile t owns slots [t*W, t*W + W),
@@ -351,8 +361,9 @@ __host__ __device__ constexpr int warp_smem_floats() {
 template <int H, class Map, int U, bool PROBE>
 __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int tile, int w,
                                              int lane) {
-    constexpr int F = Map::F;
+    constexpr int F = Map::F, S = Map::S, NR = Map::L * Map::F;   // NR: floats per tile row
     constexpr int WS = warp_smem_floats<H, Map>();
+    const int sub = lane / Map::L, lj = lane % Map::L;
     const int slot = tile * (blockDim.x >> 5) + w;
     const int aux = p.item_aux[slot];
     const int4 it = p.items[slot];   // independent of aux: both loads in flight together
@@ -372,6 +383,15 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
             walk<H, Map, U, PROBE>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y,
                                    it.z, it.w, acc, lane);
         }
+        if constexpr (S > 1) {   // warp-level reduction of the sub-warps
+#pragma unroll
+            for (int r = 0; r < H; r++)
+#pragma unroll
+                for (int f = 0; f < F; f++)
+#pragma unroll
+                    for (int off = Map::L; off < 32; off <<= 1)
+                        acc[r][f] += __shfl_xor_sync(kFull, acc[r][f], off);
+        }
     }
     __syncwarp();   // staging reads done before the area holds the partial
 
@@ -388,23 +408,24 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
         const bool heavy = (aux >> 18) & 1;
         const int cnt = (aux >> 8) & 0xff, lead = aux & 0xff;
         if (!((aux >> 17) & 1)) {   // every panel of this tile has exactly one item here
-            if (active) store_rows<H, Map>(p, panel, acc, lane);
+            if (active) store_rows<H, Map>(p, panel, acc, sub, lj);
             return;
         }
         float* mine = smem + (size_t)w * WS;
         if (active && (cnt > 1 || heavy)) {
 #pragma unroll
             for (int r = 0; r < H; r++)
+                if ((r % S) == sub)
 #pragma unroll
-                for (int f = 0; f < F; f++) {
-                    const int j = Map::col(lane, f);
-                    if (Map::kVec || j < n) mine[r * 32 * F + j] = acc[r][f];
-                }
+                    for (int f = 0; f < F; f++) {
+                        const int j = Map::col(lj, f);
+                        if (Map::kVec || j < n) mine[r * NR + j] = acc[r][f];
+                    }
         }
         __syncthreads();
         if (!active) return;
         if (cnt == 1 && !heavy) {
-            store_rows<H, Map>(p, panel, acc, lane);
+            store_rows<H, Map>(p, panel, acc, sub, lj);
             return;
         }
         if (w != lead) return;
@@ -418,14 +439,15 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
             const float* part = smem + (size_t)(lead + q) * WS;
 #pragma unroll
             for (int r = 0; r < H; r++)
+                if ((r % S) == sub)
 #pragma unroll
-                for (int f = 0; f < F; f++) {
-                    const int j = Map::col(lane, f);
-                    if (Map::kVec || j < n) acc[r][f] += part[r * 32 * F + j];
-                }
+                    for (int f = 0; f < F; f++) {
+                        const int j = Map::col(lj, f);
+                        if (Map::kVec || j < n) acc[r][f] += part[r * NR + j];
+                    }
         }
         if (!heavy) {
-            store_rows<H, Map>(p, panel, acc, lane);
+            store_rows<H, Map>(p, panel, acc, sub, lj);
             return;
         }
         // heavy panel: its tiles combine through the global workspace
@@ -434,11 +456,12 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
         float* wsq = p.ws + (size_t)(hv.y + th.y) * H * n;
 #pragma unroll
         for (int r = 0; r < H; r++)
+            if ((r % S) == sub)
 #pragma unroll
-            for (int f = 0; f < F; f++) {
-                const int j = Map::col(lane, f);
-                if (Map::kVec || j < n) __stcg(wsq + r * n + j, acc[r][f]);
-            }
+                for (int f = 0; f < F; f++) {
+                    const int j = Map::col(lj, f);
+                    if (Map::kVec || j < n) __stcg(wsq + r * n + j, acc[r][f]);
+                }
         __threadfence();
         __syncwarp();
         int last = 0;
@@ -455,13 +478,14 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
             const float* part = p.ws + (size_t)(hv.y + t) * H * n;
 #pragma unroll
             for (int r = 0; r < H; r++)
+                if ((r % S) == sub)
 #pragma unroll
-                for (int f = 0; f < F; f++) {
-                    const int j = Map::col(lane, f);
-                    if (Map::kVec || j < n) acc[r][f] += __ldcg(part + r * n + j);
-                }
+                    for (int f = 0; f < F; f++) {
+                        const int j = Map::col(lj, f);
+                        if (Map::kVec || j < n) acc[r][f] += __ldcg(part + r * n + j);
+                    }
         }
-        store_rows<H, Map>(p, hv.x, acc, lane);
+        store_rows<H, Map>(p, hv.x, acc, sub, lj);
         if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
     }
 }

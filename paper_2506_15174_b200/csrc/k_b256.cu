@@ -1,9 +1,9 @@
-// Instantiations of the ESC kernel for lane map VecMap<8> (see esc_kernel.cuh).
+// Instantiations of the ESC kernel for lane map VecMap<32, 8> (see esc_kernel.cuh).
 #include "esc_kernel.cuh"
 namespace escs {
 namespace kern {
 KernelFn get_b256(int h, int ufk, bool probe) {
-    using M = VecMap<8>;
+    using M = VecMap<32, 8>;
     if (h == 1 && ufk == 2) return probe ? esc_spmm_kernel<1, M, 2, true> : esc_spmm_kernel<1, M, 2, false>;
     if (h == 1 && ufk == 4) return probe ? esc_spmm_kernel<1, M, 4, true> : esc_spmm_kernel<1, M, 4, false>;
     if (h == 1 && ufk == 8) return probe ? esc_spmm_kernel<1, M, 8, true> : esc_spmm_kernel<1, M, 8, false>;

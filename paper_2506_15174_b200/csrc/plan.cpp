@@ -308,32 +308,35 @@ void build_tiles(PlanHost& ph, int W) {
     ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 
-// Parameter table (§3.5 Scheduler & Tuner): fitted to the
-// profiling sweep of tools/tune.py on B200 (profiles/tune_*.json).
-//  * UFi: the enumerated blocks pay (fewer gathered B rows, p = h(1-s)/(1-s^h))
-//    only at low sparsity with narrow B rows and a small, cache-resident B;
-//    otherwise the predicated pattern rows cost more than they save -> 1.
-//  * UFk: B rows in flight per warp, bounded by registers (UFk * bCols/32).
-//  * T: about 3200 items per launch (one wave of ~22 warps per SM on 148
-//    SMs, each item long enough to amortise its ~4 dependent round trips),
-//    at least 16 columns (8 for tiny problems), rounded so that a typical
-//    panel splits into equal items.
+// Parameter table (§3.5 Scheduler & Tuner), fitted to the
+// profiling sweeps of tools/tune.py on B200 (profiles/r1_tune_*.json):
+//  * UFi: the sweep over {1, 2, 4} on both layer suites picks UFi = 1 for every
+//    case (UFi = 4 is 1.1-1.9x slower): the B rows that enumeration saves
+//    (p = h(1-s)/(1-s^h) = 1.58 at 70%) hit the 126 MB L2 / large L1 anyway,
+//    while patterns add the slot indirection and predicated rows.  Explicit
+//    UFi (escs_plan_ex / ESCS_PARAMS) runs the enumerated kernel.
+//  * UFk = 8 B rows in flight per sub-warp (4 at bCols 256: registers).
+//  * T: about 1536 items per launch (~10 warps per SM on 148 SMs: each item
+//    long enough to amortise its dependent round trips), at least 16 columns,
+//    rounded (with a 3-sigma margin) so that a typical panel splits into
+//    equal items.
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
     Params p;
     const double d = (double)nnz / ((double)m * (double)k);
     const double s = 1.0 - d;
-    p.h = (s <= 0.75 && bcols <= 64 && k <= 1024) ? 4 : 1;
+    p.h = 1;
     p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
-    p.ufk = bcols <= 64 ? 8 : 4;
+    p.ufk = bcols > 128 ? 4 : 8;
     const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
-    const double target_items = 3200.0 * (double)n_sm / 148.0;
-    int64_t T = (int64_t)std::ceil(G / target_items);
-    const int64_t Tmin = G < 16.0 * 4.0 * n_sm ? 8 : 16;
-    T = std::max<int64_t>(T, Tmin);
+    const double target_items = 1536.0 * (double)n_sm / 148.0;
+    const int64_t Tmin = 16;
+    int64_t T = std::max<int64_t>(Tmin, (int64_t)std::ceil(G / target_items));
     if (sp >= 1.0) {
+        // panel streams vary around sp (binomial, sigma ~ sqrt(sp)): leave a
+        // 3-sigma margin so that typical panels really split into `per` items
         const int64_t per = std::max<int64_t>(1, (int64_t)std::ceil(sp / (double)T));
-        T = std::max<int64_t>(Tmin, (int64_t)std::ceil(sp / (double)per));
+        T = std::max<int64_t>(Tmin, (int64_t)std::ceil((sp + 3.0 * std::sqrt(sp)) / (double)per));
     }
     T = std::min<int64_t>(T, 1 << 20);
     p.T = (int)T;
