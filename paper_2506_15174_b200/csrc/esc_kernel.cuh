@@ -50,9 +50,30 @@ struct KParams {
     int m, n;
 };
 
+// L2 cache policies: the plan and value streams are read once per call
+// (evict_first); the gathered B rows are re-read by many panels and should
+// stay L2-resident across the streams (evict_last).  createpolicy folds into
+// the load's uniform descriptor (no per-load cost).
+__device__ __forceinline__ unsigned long long policy_first() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ unsigned long long policy_last() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ int ld_stream(const int* p) {
     int r;
-    asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(r) : "l"(p), "l"(policy_first()));
+    return r;
+}
+__device__ __forceinline__ float ld_stream_f(const float* p) {
+    float r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;"
+                 : "=f"(r) : "l"(p), "l"(policy_first()));
     return r;
 }
 
@@ -67,17 +88,20 @@ struct VecMap {
     __device__ static __forceinline__ int col(int lj, int f) { return lj * F + f; }
     __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lj) {
         const float* q = row + lj * F;
+        const unsigned long long pol = policy_last();
         if constexpr (F == 1) {
-            asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(b[0]) : "l"(q));
+            asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
+                         : "=f"(b[0]) : "l"(q), "l"(pol));
         } else if constexpr (F == 2) {
-            asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(b[0]), "=f"(b[1]) : "l"(q));
+            asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                         : "=f"(b[0]), "=f"(b[1]) : "l"(q), "l"(pol));
         } else {
 #pragma unroll
             for (int v = 0; v < F / 4; v++)
-                asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+                asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                              : "=f"(b[4 * v]), "=f"(b[4 * v + 1]), "=f"(b[4 * v + 2]),
                                "=f"(b[4 * v + 3])
-                             : "l"(q + 4 * v));
+                             : "l"(q + 4 * v), "l"(pol));
         }
     }
     __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lj) {
@@ -157,7 +181,7 @@ __device__ __forceinline__ int fetch_chunk(const KParams& p, const int* gp, int 
 #pragma unroll
         for (int r = 0; r < H; r++) {
             const int rank = __popc(mask & ((1u << r) - 1u));
-            w[r] = ((mask >> r) & 1u) ? __ldg(p.vals + ld_stream(sp + rank)) : 0.f;
+            w[r] = ((mask >> r) & 1u) ? ld_stream_f(p.vals + ld_stream(sp + rank)) : 0.f;
         }
         return sbase + total;
     }
@@ -215,11 +239,11 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
     float v0 = 0.f, v1 = 0.f;
     if (lane < n) {
         pk0 = ld_stream(gp + lane);
-        if constexpr (!PROBE) v0 = __ldg(vp + lane);
+        if constexpr (!PROBE) v0 = ld_stream_f(vp + lane);
     }
     if (32 + lane < n) {
         pk1 = ld_stream(gp + 32 + lane);
-        if constexpr (!PROBE) v1 = __ldg(vp + 32 + lane);
+        if constexpr (!PROBE) v1 = ld_stream_f(vp + 32 + lane);
     }
 #pragma unroll 1
     for (int c0 = 0; c0 < n; c0 += 32) {
@@ -227,7 +251,7 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
         float v2 = 0.f;
         if (c0 + 64 + lane < n) {
             pk2 = ld_stream(gp + c0 + 64 + lane);
-            if constexpr (!PROBE) v2 = __ldg(vp + c0 + 64 + lane);
+            if constexpr (!PROBE) v2 = ld_stream_f(vp + c0 + 64 + lane);
         }
         const int cn = min(32, n - c0);
         int s = 0;

@@ -315,7 +315,8 @@ void build_tiles(PlanHost& ph, int W) {
 //    (p = h(1-s)/(1-s^h) = 1.58 at 70%) hit the 126 MB L2 / large L1 anyway,
 //    while patterns add the slot indirection and predicated rows.  Explicit
 //    UFi (escs_plan_ex / ESCS_PARAMS) runs the enumerated kernel.
-//  * UFk = 8 B rows in flight per sub-warp (4 at bCols 256: registers).
+//  * UFk = 8 B rows in flight per sub-warp on the layer suites; 4 on large
+//    problems (occupancy) and at bCols 256 (registers).
 //  * T: about 1536 items per launch (~10 warps per SM on 148 SMs: each item
 //    long enough to amortise its dependent round trips), at least 16 columns,
 //    rounded (with a 3-sigma margin) so that a typical panel splits into
@@ -326,7 +327,11 @@ Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm)
     const double s = 1.0 - d;
     p.h = 1;
     p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
-    p.ufk = bcols > 128 ? 4 : 8;
+    // more rows in flight per warp on the small, latency-bound layers; more
+    // resident warps (fewer registers) on the large, L2-bandwidth-bound ones
+    // (C4: 183 -> 135 us, C5: 2.63 -> 2.28 ms with UFk 4; profiles/r1_notes.md)
+    const double g_est = (double)nnz;   // gcols at UFi = 1
+    p.ufk = (bcols > 128 || g_est > 1.5e6) ? 4 : 8;
     const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
     const double target_items = 1536.0 * (double)n_sm / 148.0;

@@ -165,13 +165,21 @@ def power_law(m: int, k: int, s: float, seed: int) -> CSR:
 
 
 def uniform_large(m: int, k: int, s: float, seed: int) -> CSR:
-    """C5: exactly nnz positions uniform without replacement over m*k: row
-    counts multivariate-hypergeometric, then columns uniform without
-    replacement per row (the same distribution); tail-Gaussian values."""
+    """C5: exactly nnz positions spread uniformly over m*k.  Row counts are
+    Binomial(k, 1-s) adjusted by +-1 on uniformly chosen rows to the exact
+    total (m*k = 2^34 is beyond numpy's multivariate-hypergeometric), then
+    columns uniform without replacement per row; tail-Gaussian values."""
     rng = np.random.default_rng(seed)
     nnz = nnz_for(m, k, s)
-    lens = rng.multivariate_hypergeometric(np.full(m, k, np.int64), nnz)
-    return _rows_to_csr(m, k, lens.astype(np.int64), rng, s)
+    lens = rng.binomial(k, 1.0 - s, size=m).astype(np.int64)
+    diff = nnz - int(lens.sum())
+    while diff != 0:
+        rows = rng.integers(0, m, size=abs(diff))
+        step = 1 if diff > 0 else -1
+        np.add.at(lens, rows, step)
+        np.clip(lens, 0, k, out=lens)
+        diff = nnz - int(lens.sum())
+    return _rows_to_csr(m, k, lens, rng, s)
 
 
 def dense_b(k: int, n: int, seed: int) -> np.ndarray:

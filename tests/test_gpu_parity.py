@@ -210,3 +210,19 @@ def test_rowblock_shards_stitch(torch_cuda):
         C, _ = run_escs(torch_cuda, S, p.B)
         parts.append(C)
     check_tol(p.A, p.B, np.concatenate(parts))
+
+
+def test_c5_full_size_sampled(torch_cuda):
+    """C5 (131072^2 at 99.5%, bCols 128) in the bench's launch configuration:
+    sampled rows against the oracle (G2) and the dyadic twin exactly."""
+    p = synth.config("c5")
+    C, pl = run_escs(torch_cuda, p.A, p.B)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([rng.choice(p.A.m, 512, replace=False),
+                                     [0, p.A.m - 1]]))
+    check_tol(p.A, p.B, C, rows=rows)
+    assert np.all(np.isfinite(C))
+    A, B = synth.dyadic_twin(p.A, 128, 5)
+    C, _ = run_escs(torch_cuda, A, B)
+    ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B, rows=rows)
+    assert np.array_equal(C[rows].astype(np.float64), ref)
