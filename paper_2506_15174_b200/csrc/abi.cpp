@@ -88,6 +88,11 @@ int auto_cta_warps(const escs::PlanHost& ph) {
     const int64_t k99 = std::min<int64_t>(nP - 1, (nP * 99) / 100);
     std::nth_element(per.begin(), per.begin() + k99, per.end());
     const int typ = std::max(1, per[k99]);
+    std::nth_element(per.begin(), per.begin() + nP / 2, per.begin() + k99);
+    const int med = std::max(1, per[nP / 2]);
+    // skewed panels (power-law rows, C4): small tiles, heavy panels combine
+    // through the workspace (C4: 117 -> 92 us with 4 warps; r1_tune_c4.json)
+    if (typ >= 4 * med) return 4;
     if (typ >= 8) return std::min(typ, 16);
     return typ * std::max(1, 8 / typ);
 }
@@ -271,6 +276,10 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
     dp.m = (int)m; dp.k = (int)k; dp.bcols = bCols; dp.h = p.h;
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
     dp.ufk = p.ufk; dp.any_sync = P->host.any_sync;
+    {
+        const char* e = std::getenv("ESCS_PDL");
+        dp.pdl = !(e && e[0] == '0');
+    }
     if (!host_only) {
         if (!upload(P)) {
             escs_free(P);

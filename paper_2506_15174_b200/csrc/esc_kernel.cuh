@@ -64,6 +64,14 @@ __device__ __forceinline__ unsigned long long policy_last() {
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// Programmatic dependent launch (PDL): the plan is immutable, so a launch may
+// read it while the previous kernel in the stream is still finishing; every
+// read of caller data (vals, B) and every write of C happens after
+// griddepcontrol.wait (the previous grid has completed and its writes are
+// visible).  No-ops when the launch carries no programmatic dependency.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ int ld_stream(const int* p) {
     int r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
@@ -237,13 +245,12 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
     const float* vp = p.vals + sbase;
     int pk0 = 0, pk1 = 0;
     float v0 = 0.f, v1 = 0.f;
-    if (lane < n) {
-        pk0 = ld_stream(gp + lane);
-        if constexpr (!PROBE) v0 = ld_stream_f(vp + lane);
-    }
-    if (32 + lane < n) {
-        pk1 = ld_stream(gp + 32 + lane);
-        if constexpr (!PROBE) v1 = ld_stream_f(vp + 32 + lane);
+    if (lane < n) pk0 = ld_stream(gp + lane);          // plan: before the PDL wait
+    if (32 + lane < n) pk1 = ld_stream(gp + 32 + lane);
+    grid_dep_wait();
+    if constexpr (!PROBE) {
+        if (lane < n) v0 = ld_stream_f(vp + lane);
+        if (32 + lane < n) v1 = ld_stream_f(vp + 32 + lane);
     }
 #pragma unroll 1
     for (int c0 = 0; c0 < n; c0 += 32) {
@@ -310,6 +317,7 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
     const int* gp = p.gpk + beg;
     int pk;
     float w[H];
+    grid_dep_wait();
     sbase = fetch_chunk<H, PROBE>(p, gp, n, 0, sbase, lane, pk, w);
     put_chunk<H>(st, 0, lane, pk, w);
     __syncwarp();
@@ -521,6 +529,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
 template <int H, class Map, int U, bool PROBE>
 __global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
     extern __shared__ __align__(16) float smem[];
+    grid_dep_launch();   // the next launch may start reading its plan
     process_tile<H, Map, U, PROBE>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31);
 }
 

@@ -60,6 +60,7 @@ struct DevPlan {
     int32_t* counters = nullptr;        // int32[n_heavy]
     int m = 0, k = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4;
     bool any_sync = false;
+    bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
 };
 
 // Launch the ESC SpMM kernel (one launch).  Returns a cudaError_t value.

@@ -56,6 +56,25 @@ kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, 
     return p;
 }
 
+// One launch; with programmatic stream serialization (PDL) unless disabled
+// (ESCS_PDL=0), so that the launch's plan reads overlap the previous kernel.
+int launch(kern::KernelFn fn, const DevPlan& dp, const kern::KParams& p, size_t smem,
+           void* stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(dp.n_tiles);
+    cfg.blockDim = dim3(32 * dp.cta_warps);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = dp.pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, fn, p);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
 }  // namespace
 
 bool kernel_supported(int h, int bcols, int variant, int ufk) {
@@ -124,8 +143,7 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, vals, B, C);
-    fn<<<dp.n_tiles, 32 * dp.cta_warps, smem_for(dp, vec), (cudaStream_t)stream>>>(p);
-    return (int)cudaGetLastError();
+    return launch(fn, dp, p, smem_for(dp, vec), stream);
 }
 
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok) {
@@ -134,8 +152,7 @@ int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, b
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, nullptr, B, sink);
-    fn<<<dp.n_tiles, 32 * dp.cta_warps, smem_for(dp, true), (cudaStream_t)stream>>>(p);
-    return (int)cudaGetLastError();
+    return launch(fn, dp, p, smem_for(dp, true), stream);
 }
 
 }  // namespace escs
