@@ -314,14 +314,30 @@ def run_escs(args):
     from paper_2506_15174_b200 import escs, shard
 
     problems, desc = workload(args.workload)
-    # row-block shard of every problem; world = 1 -> whole problem
+    # N > 1: a suite of independent problems is partitioned over ranks (LPT by
+    # flops, no collective); a single large problem is row-block sharded with
+    # B replicated.  N = 1: every problem whole.
+    mode = args.shard
+    if mode == "auto":
+        mode = "problems" if len(problems) >= 2 * world else "rows"
+    if world > 1 and mode == "problems":
+        mine = shard.partition_problems([p.flops for p in problems], world)[rank]
+        sharding = f"problems (LPT by flops) x{world}"
+    else:
+        mine = list(range(len(problems)))
+        sharding = f"row-block x{world}"
     dev = {"_device": device}
     shard_problems = []
     plan_s = 0.0
     plan_info = []
-    for p in problems:
+    for idx in mine:
+        p = problems[idx]
         t0 = time.perf_counter()
-        A, pl = shard.plan_shard(p.A, p.bcols, world, rank)
+        if mode == "problems":
+            A = p.A
+            pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols)
+        else:
+            A, pl = shard.plan_shard(p.A, p.bcols, world, rank)
         plan_s += time.perf_counter() - t0
         info = pl.info
         plan_info.append(info)
@@ -430,7 +446,7 @@ def run_escs(args):
 
     # ---- optional all-gather of C (NCCL), timed separately (not on the hot path)
     allgather_ms = None
-    if world > 1 and args.allgather:
+    if world > 1 and args.allgather and mode == "rows":
         ga, gb = ev(), ev()
         barrier()
         ga.record(stream)
@@ -462,7 +478,7 @@ def run_escs(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "problems": nprob, "sharding": f"row-block x{world}",
+            "config": {"workload": desc, "problems": len(problems), "sharding": sharding,
                        "l2": "flushed before every step (256 MiB write); each problem touched once per step",
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "variant")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -479,7 +495,7 @@ def run_escs(args):
                              "probe_ms_per_step": probe_ms / K,
                              "frac": probe_ms / float(kern_ms.sum()),
                              "what": "t_probe / t_kernel: escs_gather_probe runs the same item walk and B-row gathers without values or FMAs (measured gather ceiling of this plan)"}},
-            "gpu_launches": nprob * K,
+            "gpu_launches": nprob * K,   # this rank's escs_spmm launches in the timed region
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -516,6 +532,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--cases-out", default=None)
+    ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],
+                    help="N>1: partition a suite by problems or row-block shard every problem")
     ap.add_argument("--allgather", action="store_true",
                     help="N>1: also time the optional NCCL all-gather of C (not on the hot path)")
     args = ap.parse_args(argv)

@@ -87,7 +87,11 @@ escs_plan_t escs_plan(int64_t m, int64_t k, int64_t nnz,
  *   stream cudaStream_t (as void*), may be NULL.
  *
  * Exactly one kernel launch, enqueue-only: no host synchronisation, no
- * allocation, no memset -- capturable in a CUDA graph.  Two calls on the same
+ * allocation, no memset -- capturable in a CUDA graph.  The launch uses
+ * programmatic dependent launch: it may start reading its (immutable) plan
+ * while the previous kernel in `stream` finishes, but reads vals/B and writes
+ * C only after that kernel has completed (stream order is preserved for the
+ * caller's data; set ESCS_PDL=0 to launch without the attribute).  Two calls on the same
  * plan must not be in flight concurrently (they share the plan's fixup
  * workspace).  Asynchronous device faults surface at the next synchronising
  * CUDA call, as with cuBLAS.  Pointers that are not 16-byte aligned take the
@@ -158,6 +162,8 @@ typedef struct {
     int64_t device_bytes;   /* plan arrays + workspace resident on the device     */
     int64_t workspace_bytes;
     double plan_seconds;    /* host enumeration time                              */
+    int32_t ctas_per_sm;    /* resident CTAs per SM of the launch (occupancy), 0 host-only */
+    int32_t reserved;
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);

@@ -45,13 +45,6 @@ int sm_count_of_current_device() {
     return n > 0 ? n : 148;
 }
 
-bool env_sets(const char* key) {
-    const char* e = std::getenv("ESCS_PARAMS");
-    if (!e) return false;
-    std::string s = std::string(",") + e, k = std::string(",") + key + "=";
-    return s.find(k) != std::string::npos;
-}
-
 // ESCS_PARAMS="ufi=4,T=64,warps=8,variant=1,ufk=4"
 void apply_env(escs::Params& p, bool& set_warps) {
     const char* e = std::getenv("ESCS_PARAMS");
@@ -391,6 +384,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->device_bytes = (int64_t)plan->dbytes;
     o->workspace_bytes = (int64_t)plan->ws_bytes;
     o->plan_seconds = h.plan_seconds;
+    o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false);
     return ESCS_OK;
 }
 

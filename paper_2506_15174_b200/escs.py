@@ -46,7 +46,8 @@ class _Stats(ctypes.Structure):
                                               "n_tiles", "n_heavy", "n_split_items", "device")] + \
                [(n, ctypes.c_int64) for n in ("nP", "NG", "G", "n_items", "nnz", "device_bytes",
                                               "workspace_bytes")] + \
-               [("plan_seconds", ctypes.c_double)]
+               [("plan_seconds", ctypes.c_double), ("ctas_per_sm", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -211,7 +212,7 @@ def escs_plan_info(plan: Plan) -> dict:
     s = _Stats()
     if _lib.escs_plan_info(plan.handle, ctypes.byref(s)) != ESCS_OK:
         _raise_last()
-    return {n: getattr(s, n) for n, _ in _Stats._fields_}
+    return {n: getattr(s, n) for n, _ in _Stats._fields_ if n != "reserved"}
 
 
 def spmm(plan: Plan, vals, B, C=None, stream=None):

@@ -31,6 +31,21 @@ def plan_shard(A: "synth.CSR", bcols: int, world: int, rank: int, **params):
     return S, escs.escs_plan(S.m, S.k, S.nnz, S.rowptr, S.colidx, bcols)
 
 
+def partition_problems(costs, world: int):
+    """Independent problems (a layer suite) over ranks: longest-processing-
+    time-first greedy on the given costs (e.g. flops), deterministic (ties by
+    index, then lowest rank).  Returns one list of problem indices per rank,
+    each in ascending order."""
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0.0] * world
+    out = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        out[r].append(i)
+        load[r] += costs[i]
+    return [sorted(x) for x in out]
+
+
 def all_gather_rows(C_local, m: int, world: int, group=None):
     """Optional all-gather of the C row blocks into the full m x n C on every
     rank.  Row blocks may differ by one row; they are padded to the largest

@@ -77,3 +77,16 @@ def test_shard_bounds_cover_rows():
             assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
             sizes = [b - a for a, b in blocks]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_partition_problems_lpt():
+    from paper_2506_15174_b200 import shard, synth
+    costs = [p.flops for p in synth.transformer_suite()]
+    for world in (1, 2, 4, 8):
+        parts = shard.partition_problems(costs, world)
+        flat = sorted(i for part in parts for i in part)
+        assert flat == list(range(len(costs)))          # every problem exactly once
+        loads = [sum(costs[i] for i in part) for part in parts]
+        # LPT bound: max load <= mean + largest single cost
+        assert max(loads) <= sum(costs) / world + max(costs)
+        assert parts == shard.partition_problems(costs, world)   # deterministic

@@ -226,3 +226,32 @@ def test_c5_full_size_sampled(torch_cuda):
     C, _ = run_escs(torch_cuda, A, B)
     ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B, rows=rows)
     assert np.array_equal(C[rows].astype(np.float64), ref)
+
+
+def test_pdl_stream_order_with_neighbours(torch_cuda):
+    """escs_spmm overlaps its plan reads with the previous kernel (PDL) but
+    must see B/vals written by that kernel and finish C before the next one
+    reads it: write B and vals with torch kernels right before the call, read
+    C right after, on the same stream, many times back to back."""
+    torch = torch_cuda
+    from paper_2506_15174_b200 import escs
+    A0 = synth.magnitude_pruned(2048, 512, 0.9, 21)
+    A, B = synth.dyadic_twin(A0, 64, 22)
+    pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        dB = torch.zeros(A.k, 64, device="cuda")
+        dv = torch.zeros(A.nnz, device="cuda")
+        src_B = torch.from_numpy(B).cuda()
+        src_v = torch.from_numpy(A.vals).cuda()
+        C = torch.empty(A.m, 64, device="cuda")
+        outs = []
+        for it in range(6):
+            dB.copy_(src_B * float(it + 1))     # kernel writing B just before the call
+            dv.copy_(src_v)
+            escs.escs_spmm(pl, dv, dB, C, stream=s)
+            outs.append(C.clone())              # kernel reading C right after
+    torch.cuda.synchronize()
+    ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B)
+    for it, c in enumerate(outs):
+        assert np.array_equal(c.cpu().numpy().astype(np.float64), ref * (it + 1))
