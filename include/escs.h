@@ -101,6 +101,28 @@ escs_plan_t escs_plan(int64_t m, int64_t k, int64_t nnz,
 int escs_spmm(escs_plan_t plan, const float *vals, const float *B, float *C,
               void *stream);
 
+/*
+ * escs_pack -- the value half of the paper's data transformation ("ANNZ":
+ * the nonzeros re-stored in kernel traversal order, §3.3.3; built
+ * once and reused across inference calls): packed[s] =
+ * vals[slot_src[s]] for s < nnz (Reading R1 slot order).  One kernel launch
+ * on `stream`, enqueue-only.
+ *   vals    DEVICE float[nnz], CSR order.
+ *   packed  DEVICE float[nnz], caller-owned output, must not alias vals.
+ * Returns ESCS_OK, ESCS_ERR_ARG or ESCS_ERR_CUDA.
+ */
+int escs_pack(escs_plan_t plan, const float *vals, float *packed, void *stream);
+
+/*
+ * escs_spmm_packed -- escs_spmm with values already packed by escs_pack: the
+ * kernel reads each chunk's values contiguously instead of through slot_src
+ * (one dependent load fewer per chunk at UFi > 1; identical to escs_spmm at
+ * UFi = 1, whose slot map is the identity).  Same contract as escs_spmm;
+ * the result is bitwise identical to escs_spmm on the unpacked values.
+ */
+int escs_spmm_packed(escs_plan_t plan, const float *packed, const float *B, float *C,
+                     void *stream);
+
 /* Release the plan's host and device memory.  NULL is a no-op.  No call on
  * the plan may be in flight. */
 void escs_free(escs_plan_t plan);

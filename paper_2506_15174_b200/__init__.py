@@ -7,13 +7,14 @@ without the CUDA library; any compute call fails loudly if the library is
 missing.
 """
 __all__ = ["escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
-           "escs_plan_export", "Plan", "spmm", "synth"]
+           "escs_plan_export", "escs_plan_info", "escs_pack", "escs_spmm_packed",
+           "escs_gather_probe", "Plan", "spmm", "synth", "shard"]
 
 
 def __getattr__(name):
-    if name == "synth":
+    if name in ("synth", "shard"):
         import importlib
-        return importlib.import_module(__name__ + ".synth")
+        return importlib.import_module(__name__ + "." + name)
     if name in __all__:
         import importlib
         return getattr(importlib.import_module(__name__ + ".escs"), name)

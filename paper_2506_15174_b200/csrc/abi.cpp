@@ -266,7 +266,7 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
     P->host_only = host_only;
     P->device = device;
     auto& dp = P->dev;
-    dp.m = (int)m; dp.k = (int)k; dp.bcols = bCols; dp.h = p.h;
+    dp.m = (int)m; dp.k = (int)k; dp.nnz = (int)nnz; dp.bcols = bCols; dp.h = p.h;
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
     dp.ufk = p.ufk; dp.any_sync = P->host.any_sync;
     {
@@ -305,7 +305,8 @@ escs_plan_t escs_plan_ex(int64_t m, int64_t k, int64_t nnz, const int32_t* rowpt
     return make_plan(m, k, nnz, rowptr, colidx, bCols, p);
 }
 
-int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, void* stream) {
+static int spmm_common(escs_plan_t plan, const float* vals, const float* B, float* C,
+                       void* stream, bool packed) {
     clear_error();
     if (!plan) return fail(ESCS_ERR_ARG, "plan is NULL");
     if (plan->host_only) return fail(ESCS_ERR_ARG, "plan is host-only (escs_params.host_only=1)");
@@ -317,8 +318,30 @@ int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, voi
                                       " differs from the plan's device " +
                                       std::to_string(plan->device));
     const bool vec_ok = aligned16(B) && aligned16(C);
-    int e = escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok);
+    int e = escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok, packed);
     if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
+                                          cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
+int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, void* stream) {
+    return spmm_common(plan, vals, B, C, stream, false);
+}
+
+int escs_spmm_packed(escs_plan_t plan, const float* packed, const float* B, float* C,
+                     void* stream) {
+    return spmm_common(plan, packed, B, C, stream, true);
+}
+
+int escs_pack(escs_plan_t plan, const float* vals, float* packed, void* stream) {
+    clear_error();
+    if (!plan || plan->host_only) return fail(ESCS_ERR_ARG, "plan is NULL or host-only");
+    if (plan->host.header[3] > 0 && (!vals || !packed))
+        return fail(ESCS_ERR_ARG, "vals and packed must be non-NULL device pointers");
+    if (vals == packed && plan->host.header[3] > 0)
+        return fail(ESCS_ERR_ARG, "packed must not alias vals");
+    int e = escs::launch_pack(plan->dev, vals, packed, stream);
+    if (e) return fail(ESCS_ERR_CUDA, std::string("pack launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
     return ESCS_OK;
 }

@@ -44,6 +44,7 @@ struct KParams {
     const int4* __restrict__ heavy;    // panel, ws_base, ntiles, 0
     float* ws;
     int* counters;                     // heavy-panel arrival counters
+    int packed;                        // vals already in slot order (escs_pack)
     const float* __restrict__ vals;
     const float* __restrict__ B;
     float* __restrict__ C;
@@ -185,11 +186,16 @@ __device__ __forceinline__ int fetch_chunk(const KParams& p, const int* gp, int 
             excl += __popc(bal & lt) << bit;
             total += __popc(bal) << bit;
         }
+        // packed values (escs_pack, the paper's ANNZ) are read contiguously;
+        // CSR-ordered values through the slot map
         const int* sp = p.slot + sbase + excl;
+        const float* pv = p.vals + sbase + excl;
 #pragma unroll
         for (int r = 0; r < H; r++) {
             const int rank = __popc(mask & ((1u << r) - 1u));
-            w[r] = ((mask >> r) & 1u) ? ld_stream_f(p.vals + ld_stream(sp + rank)) : 0.f;
+            float x = 0.f;
+            if ((mask >> r) & 1u) x = ld_stream_f(p.packed ? pv + rank : p.vals + ld_stream(sp + rank));
+            w[r] = x;
         }
         return sbase + total;
     }

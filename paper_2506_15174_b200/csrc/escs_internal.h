@@ -58,14 +58,16 @@ struct DevPlan {
     const int32_t* heavy = nullptr;     // int4[n_heavy]
     float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
     int32_t* counters = nullptr;        // int32[n_heavy]
-    int m = 0, k = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4;
+    int m = 0, k = 0, nnz = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
 };
 
 // Launch the ESC SpMM kernel (one launch).  Returns a cudaError_t value.
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
-                bool vec_ok);
+                bool vec_ok, bool packed = false);
+// escs_pack: packed[s] = vals[slot[s]].
+int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream);
 // Launch the gather probe (same walk, loads only).
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok);
 // Prepare kernel attributes (dynamic smem limits) once per plan.

@@ -18,6 +18,18 @@ KernelFn get_s4(int, int, bool);
 KernelFn get_s8(int, int, bool);
 }  // namespace kern
 
+namespace kern {
+// escs_pack: packed[s] = vals[slot[s]] (the paper's ANNZ, §3.3.3).
+__global__ void __launch_bounds__(256) esc_pack_kernel(const int* __restrict__ slot,
+                                                       const float* __restrict__ vals,
+                                                       float* __restrict__ out, int nnz) {
+    grid_dep_wait();
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nnz; s += gridDim.x * blockDim.x)
+        out[s] = vals[ld_stream(slot + s)];
+}
+
+}  // namespace kern
+
 namespace {
 
 kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
@@ -38,8 +50,10 @@ kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
     return nullptr;
 }
 
-kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C) {
+kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C,
+                          bool packed = false) {
     kern::KParams p;
+    p.packed = packed ? 1 : 0;
     p.gpk = dp.gpk;
     p.slot = dp.slot;
     p.items = reinterpret_cast<const int4*>(dp.items);
@@ -136,13 +150,22 @@ int blocks_per_sm(const DevPlan& dp, bool vec, bool probe) {
     return nb > 0 ? nb : 1;
 }
 
+int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream) {
+    if (dp.nnz == 0) return 0;
+    const int threads = 256;
+    const int blocks = (int)std::min<long>(((long)dp.nnz + threads - 1) / threads, 148L * 16);
+    kern::esc_pack_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(dp.slot, vals, packed,
+                                                                          dp.nnz);
+    return (int)cudaGetLastError();
+}
+
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
-                bool vec_ok) {
+                bool vec_ok, bool packed) {
     const bool vec = vec_ok && dp.variant == 1;
     kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
-    kern::KParams p = make_params(dp, vals, B, C);
+    kern::KParams p = make_params(dp, vals, B, C, packed);
     return launch(fn, dp, p, smem_for(dp, vec), stream);
 }
 

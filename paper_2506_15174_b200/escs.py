@@ -21,7 +21,8 @@ HEADER_FIELDS = ("version", "m", "k", "nnz", "bCols", "h", "T", "nP", "NG", "G",
 PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "slot_src",
                "item_panel", "item_group_begin", "item_gcol_ptr")
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
-                    "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version")
+                    "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
+                    "escs_pack", "escs_spmm_packed")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -57,6 +58,10 @@ _lib.escs_plan_ex.argtypes = [_i64, _i64, _i64, _vp, _vp, _i32, ctypes.POINTER(_
 _lib.escs_plan_ex.restype = _vp
 _lib.escs_spmm.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.escs_spmm.restype = ctypes.c_int
+_lib.escs_spmm_packed.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.escs_spmm_packed.restype = ctypes.c_int
+_lib.escs_pack.argtypes = [_vp, _vp, _vp, _vp]
+_lib.escs_pack.restype = ctypes.c_int
 _lib.escs_gather_probe.argtypes = [_vp, _vp, _vp, _vp]
 _lib.escs_gather_probe.restype = ctypes.c_int
 _lib.escs_free.argtypes = [_vp]
@@ -177,6 +182,20 @@ def escs_spmm(plan: Plan, vals, B, C, stream=None) -> None:
     if vals is not None and not isinstance(vals, int) and vals.numel() < plan.nnz:
         raise EscsError(ESCS_ERR_ARG, f"vals must have at least nnz = {plan.nnz} elements")
     rc = _lib.escs_spmm(plan.handle, _ptr(vals), _ptr(B), _ptr(C), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+def escs_pack(plan: Plan, vals, packed, stream=None) -> None:
+    """packed[s] = vals[slot_src[s]] on the device (the paper's ANNZ)."""
+    rc = _lib.escs_pack(plan.handle, _ptr(vals), _ptr(packed), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+def escs_spmm_packed(plan: Plan, packed, B, C, stream=None) -> None:
+    """C = A x B with values pre-packed by escs_pack."""
+    rc = _lib.escs_spmm_packed(plan.handle, _ptr(packed), _ptr(B), _ptr(C), _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
 

@@ -290,3 +290,17 @@ def test_partition_determinism():
     b = oracle.partition(A.m, A.k, A.rowptr, A.colidx, 4, 10)
     for name in oracle.PLAN_ARRAYS:
         assert np.array_equal(a[name], b[name])
+
+
+def test_storage_trend_matches_paper_fig9():
+    # P:796-798 / P:823 (Fig. 9): the ESC format (ANNZ + Cols + RPP + NPP) is
+    # smaller than CSR for roughly 50-80% sparsity, and CSR is smaller near 99%.
+    m = k = 512
+    for s, esc_smaller in ((0.5, True), (0.6, True), (0.7, True), (0.8, True),
+                           (0.95, False), (0.99, False)):
+        A = synth.magnitude_pruned(m, k, s, 77)
+        p = oracle.partition(m, k, A.rowptr, A.colidx, 4, 1 << 20)
+        hdr = p["header"]
+        esc = 4 * hdr["nnz"] + 4 * hdr["G"] + 8 * (hdr["NG"] + 1) + 8 * hdr["NG"]
+        csr = 8 * A.nnz + 4 * (m + 1)
+        assert (esc < csr) == esc_smaller, (s, esc, csr)
