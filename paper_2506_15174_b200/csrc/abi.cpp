@@ -71,7 +71,11 @@ void apply_env(escs::Params& p, bool& set_warps) {
 
 // Warps per CTA tile: at least the number of items of all but the heaviest 1%
 // of panels (so they combine inside one CTA), rounded up to a multiple that
-// gives about 8 warps per CTA; at most 16.
+// gives about 8 warps per CTA; at most 16.  Skewed panels (power-law rows,
+// C4: p99 items >= 4x median) get 4-warp tiles and combine heavy panels
+// through the workspace (C4: 117 -> 92 us, profiles/r1_tune_c4.json).
+// (16-warp tiles packing several panels were measured too: faster only when
+// they remove a second wave, slower otherwise -- profiles/r1_tune_big.json.)
 int auto_cta_warps(const escs::PlanHost& ph) {
     const int64_t nP = ph.header[7];
     const int64_t NI = ph.item_panel.size();
@@ -83,8 +87,6 @@ int auto_cta_warps(const escs::PlanHost& ph) {
     const int typ = std::max(1, per[k99]);
     std::nth_element(per.begin(), per.begin() + nP / 2, per.begin() + k99);
     const int med = std::max(1, per[nP / 2]);
-    // skewed panels (power-law rows, C4): small tiles, heavy panels combine
-    // through the workspace (C4: 117 -> 92 us with 4 warps; r1_tune_c4.json)
     if (typ >= 4 * med) return 4;
     if (typ >= 8) return std::min(typ, 16);
     return typ * std::max(1, 8 / typ);

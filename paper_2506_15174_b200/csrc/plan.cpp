@@ -319,8 +319,8 @@ void build_tiles(PlanHost& ph, int W) {
 //    problems (occupancy) and at bCols 256 (registers).
 //  * T: about 1536 items per launch (~10 warps per SM on 148 SMs: each item
 //    long enough to amortise its dependent round trips), at least 16 columns,
-//    rounded (with a 3-sigma margin) so that a typical panel splits into
-//    equal items.
+//    rounded (with a 3-sigma margin on the panel stream) so that a typical
+//    panel splits into equal items.
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
     Params p;
     const double d = (double)nnz / ((double)m * (double)k);

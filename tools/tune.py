@@ -23,11 +23,17 @@ def main():
     ap.add_argument("--ufk", default="2,4,8")
     ap.add_argument("--T", default="0,8,16,32,64,128,256")
     ap.add_argument("--warps", default="0")
+    ap.add_argument("--filter", default="", help="comma-separated substrings of case names")
     a = ap.parse_args()
     import torch
     import bench
     from paper_2506_15174_b200 import escs
     problems, _ = bench.workload(a.workload)
+    if a.filter:
+        keys = a.filter.split(",")
+        problems = [p for p in problems if any(k in p.name for k in keys)]
+        seen = set()
+        problems = [p for p in problems if not (p.name in seen or seen.add(p.name))]
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     out = []
