@@ -333,11 +333,12 @@ def run_escs(args):
     for idx in mine:
         p = problems[idx]
         t0 = time.perf_counter()
+        tune = {"autotune": 1} if args.autotune else {}
         if mode == "problems":
             A = p.A
-            pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols)
+            pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, **tune)
         else:
-            A, pl = shard.plan_shard(p.A, p.bcols, world, rank)
+            A, pl = shard.plan_shard(p.A, p.bcols, world, rank, **tune)
         plan_s += time.perf_counter() - t0
         info = pl.info
         plan_info.append(info)
@@ -480,6 +481,8 @@ def run_escs(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "problems": len(problems), "sharding": sharding,
                        "l2": "flushed before every step (256 MiB write); each problem touched once per step",
+                       "plans": ("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates)"
+                                 if args.autotune else "parameter table (escs_plan defaults)"),
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "variant")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
@@ -532,6 +535,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=8.0)
     ap.add_argument("--cases-out", default=None)
+    ap.add_argument("--no-autotune", dest="autotune", action="store_false",
+                    help="plan with the parameter table only (default: plan-time autotuning)")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],
                     help="N>1: partition a suite by problems or row-block shard every problem")
     ap.add_argument("--allgather", action="store_true",

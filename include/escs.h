@@ -145,7 +145,14 @@ typedef struct {
     int32_t variant;      /* 0 = auto, 1 = vector (float4) kernel, 2 = scalar    */
     int32_t ufk;          /* B-row loads in flight per warp (UFk: 4 or 8), 0 = auto */
     int32_t nthreads;     /* planner threads, 0 = hardware concurrency           */
-    int32_t reserved[5];  /* must be zero                                        */
+    int32_t autotune;     /* 1: time candidate (T, tile width, UFk) plans on the
+                             device at plan time and keep the fastest (the
+                             paper's profiling-based tuner, §3.5);
+                             parameters given explicitly are not searched.
+                             Adds a few ms to escs_plan; the plan arrays are
+                             still the canonical plan of the chosen (UFi, T).
+                             Also enabled by ESCS_AUTOTUNE=1.                  */
+    int32_t reserved[4];  /* must be zero                                        */
 } escs_params;
 
 /* escs_plan with explicit parameters; p may be NULL (= all auto). */
@@ -185,7 +192,7 @@ typedef struct {
     int64_t workspace_bytes;
     double plan_seconds;    /* host enumeration time                              */
     int32_t ctas_per_sm;    /* resident CTAs per SM of the launch (occupancy), 0 host-only */
-    int32_t reserved;
+    int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);

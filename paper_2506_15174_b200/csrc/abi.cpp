@@ -21,6 +21,7 @@ struct escs_plan_impl {
     int device = -1;
     void* dmem = nullptr;
     size_t dbytes = 0, ws_bytes = 0;
+    bool autotuned = false;
 };
 
 namespace {
@@ -182,8 +183,8 @@ bool upload(escs_plan_impl* P) {
     return true;
 }
 
-escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
-                      const int32_t* colidx, int32_t bCols, const escs_params* ep) {
+escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                            const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     clear_error();
     if (m < 1 || k < 1 || nnz < 0 || bCols < 1) {
         fail(ESCS_ERR_ARG, "m, k, bCols must be >= 1 and nnz >= 0");
@@ -199,7 +200,7 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
         return nullptr;
     }
     if (ep) {
-        for (int i = 0; i < 5; i++)
+        for (int i = 0; i < 4; i++)
             if (ep->reserved[i] != 0) {
                 fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
                 return nullptr;
@@ -292,6 +293,135 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---------------------------------------------------------------- autotune
+// The paper's scheduler & tuner (§3.5) is profiling-based: here the
+// profiling runs at plan time, on the device the plan is bound to, for this
+// matrix and bCols.  Coordinate descent over the item size T (with the auto
+// tile width), then the tile width W, then UFk; every candidate is a complete
+// canonical plan, timed as back-to-back launches (min over 3 batches of 8).
+struct TuneBufs {
+    float *vals = nullptr, *B = nullptr, *C = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    bool ok = false;
+    TuneBufs(int64_t m, int64_t k, int64_t nnz, int32_t n) {
+        ok = cudaMalloc(&vals, std::max<int64_t>(nnz, 1) * 4) == cudaSuccess &&
+             cudaMalloc(&B, (size_t)k * n * 4) == cudaSuccess &&
+             cudaMalloc(&C, (size_t)m * n * 4) == cudaSuccess &&
+             cudaMemset(vals, 0, std::max<int64_t>(nnz, 1) * 4) == cudaSuccess &&
+             cudaMemset(B, 0, (size_t)k * n * 4) == cudaSuccess &&
+             cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
+             cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+    }
+    ~TuneBufs() {
+        if (vals) cudaFree(vals);
+        if (B) cudaFree(B);
+        if (C) cudaFree(C);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (stream) cudaStreamDestroy(stream);
+        cudaGetLastError();
+    }
+};
+
+float time_plan(escs_plan_t P, TuneBufs& b) {
+    float best = 1e30f;
+    const bool vec = aligned16(b.B) && aligned16(b.C);
+    for (int w = 0; w < 2; w++) escs::launch_spmm(P->dev, b.vals, b.B, b.C, b.stream, vec);
+    for (int rep = 0; rep < 3; rep++) {
+        cudaEventRecord(b.e0, b.stream);
+        for (int i = 0; i < 8; i++) escs::launch_spmm(P->dev, b.vals, b.B, b.C, b.stream, vec);
+        cudaEventRecord(b.e1, b.stream);
+        if (cudaEventSynchronize(b.e1) != cudaSuccess) return 1e30f;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, b.e0, b.e1);
+        best = std::min(best, ms / 8);
+    }
+    return best;
+}
+
+escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                                const int32_t* colidx, int32_t bCols, const escs_params* ep) {
+    escs_params q = ep ? *ep : escs_params{};
+    q.autotune = 0;
+    escs_plan_t best = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+    if (!best || nnz > 8000000) return best;   // large problems: many waves, heuristic holds
+    TuneBufs bufs(m, k, nnz, bCols);
+    if (!bufs.ok) return best;
+    float tb = time_plan(best, bufs);
+    auto consider = [&](escs_params c) {
+        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+        if (!P) {
+            clear_error();
+            return;
+        }
+        const float t = time_plan(P, bufs);
+        if (t < tb) {
+            escs_free(best);
+            best = P;
+            tb = t;
+        } else {
+            escs_free(P);
+        }
+    };
+    const int h = best->params.h;
+    // stage 1: item size T (tile width follows automatically)
+    if (!(ep && ep->T)) {
+        const double nP = (double)best->host.header[7];
+        const double sp = nP > 0 ? (double)best->host.header[9] / nP : 0.0;
+        std::vector<int> cand;
+        const int T0 = best->params.T;
+        for (double f : {0.35, 0.5, 0.7, 1.4, 2.0, 3.0}) cand.push_back(std::max(8, (int)(T0 * f)));
+        for (int per : {1, 2, 3, 4, 6, 8})
+            if (sp >= 1.0) cand.push_back(std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / per)));
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        for (int T : cand) {
+            if (T == T0) continue;
+            escs_params c = q;
+            c.ufi = h;
+            c.T = T;
+            consider(c);
+        }
+    }
+    // stage 2: tile width
+    if (!(ep && ep->cta_warps)) {
+        const int W0 = best->params.cta_warps, T = best->params.T;
+        for (int W : {4, 8, 16}) {
+            if (W == W0) continue;
+            escs_params c = q;
+            c.ufi = h;
+            c.T = T;
+            c.cta_warps = W;
+            consider(c);
+        }
+    }
+    // stage 3: rows in flight
+    if (!(ep && ep->ufk)) {
+        const int U0 = best->params.ufk;
+        for (int U : {4, 8}) {
+            if (U == U0) continue;
+            escs_params c = q;
+            c.ufi = h;
+            c.T = best->params.T;
+            c.cta_warps = best->params.cta_warps;
+            c.ufk = U;
+            consider(c);
+        }
+    }
+    best->autotuned = true;
+    clear_error();
+    return best;
+}
+
+escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, int32_t bCols, const escs_params* ep) {
+    const char* env = std::getenv("ESCS_AUTOTUNE");
+    const bool tune = (ep && ep->autotune) || (env && env[0] == '1');
+    if (!tune || (ep && ep->host_only)) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, ep);
+    return make_plan_autotuned(m, k, nnz, rowptr, colidx, bCols, ep);
+}
 
 }  // namespace
 
@@ -410,6 +540,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->workspace_bytes = (int64_t)plan->ws_bytes;
     o->plan_seconds = h.plan_seconds;
     o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false);
+    o->autotuned = plan->autotuned ? 1 : 0;
     return ESCS_OK;
 }
 

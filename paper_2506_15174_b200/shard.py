@@ -26,6 +26,7 @@ def plan_shard(A: "synth.CSR", bcols: int, world: int, rank: int, **params):
     """escs plan of this rank's row block (host-only when params say so)."""
     from . import escs
     S = shard_matrix(A, world, rank)
+    params = {k: v for k, v in params.items() if v}
     if params:
         return S, escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, bcols, **params)
     return S, escs.escs_plan(S.m, S.k, S.nnz, S.rowptr, S.colidx, bcols)

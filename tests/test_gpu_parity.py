@@ -279,3 +279,21 @@ def test_pack_then_packed_spmm_bitwise(torch_cuda, ufi):
     assert np.array_equal(packed.cpu().numpy(), A.vals[slot])
     assert torch.equal(C1, C2)
     check_tol(A, B, C2.cpu().numpy())
+
+
+def test_autotuned_plan_parity(torch_cuda):
+    """An autotuned plan is still the canonical plan of its (UFi, T) -- byte
+    identical to the oracle partitioner given that header -- and exact."""
+    from paper_2506_15174_b200 import escs
+    A0 = synth.magnitude_pruned(512, 2048, 0.9, 41)
+    A, B = synth.dyadic_twin(A0, 64, 42)
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, autotune=1)
+    info = pl.info
+    assert info["autotuned"] == 1
+    got = pl.export()
+    ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, info["h"], info["T"], bCols=64)
+    for n in oracle.PLAN_ARRAYS:
+        assert np.array_equal(got[n], ref[n]), n
+    C, _ = run_escs(torch_cuda, A, B, ufi=info["h"], T=info["T"], cta_warps=info["cta_warps"],
+                    ufk=info["ufk"])
+    check_exact(A, B, C)
