@@ -18,14 +18,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libescs.so")
+BUILD = os.environ.get("ESCS_BUILD_DIR") or os.path.join(HERE, "build")
+LIB = os.environ.get("ESCS_LIB") or os.path.join(HERE, "libescs.so")
 BENCH_LIB = os.path.join(HERE, "libescs_bench.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                  "-Xptxas", "-v", "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+                  "-Xptxas", "-v", "-I", CSRC, "-I", os.path.join(ROOT, "include")] + \
+    os.environ.get("ESCS_NVFLAGS", "").split()       # extra flags for A/B experiment builds
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function",
             "-I", os.path.join(CUDA, "include"), "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 

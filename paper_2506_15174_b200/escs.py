@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libescs.so")
+LIB_PATH = os.environ.get("ESCS_LIB") or os.path.join(_HERE, "libescs.so")   # ESCS_LIB: A/B experiments
 
 ESCS_OK, ESCS_ERR_ARG, ESCS_ERR_CSR, ESCS_ERR_UNSUPPORTED, ESCS_ERR_OOM, ESCS_ERR_CUDA, \
     ESCS_ERR_INTERNAL = range(7)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--T", default="0,8,16,32,64,128,256")
     ap.add_argument("--warps", default="0")
     ap.add_argument("--filter", default="", help="comma-separated substrings of case names")
+    ap.add_argument("--packed", action="store_true", help="time escs_spmm_packed (values pre-packed)")
     a = ap.parse_args()
     import torch
     import bench
@@ -59,8 +60,13 @@ def main():
                                                    ufi=ufi, ufk=ufk, T=T, cta_warps=w)
                         except escs.EscsError:
                             continue
-                        t = bench.graph_time(torch, lambda: escs.escs_spmm(pl, dv, dB, dC, stream),
-                                             stream, min_ms=1.0, reps=5)
+                        if a.packed:
+                            pv = torch.empty_like(dv)
+                            escs.escs_pack(pl, dv, pv, stream)
+                            fn = lambda: escs.escs_spmm_packed(pl, pv, dB, dC, stream)
+                        else:
+                            fn = lambda: escs.escs_spmm(pl, dv, dB, dC, stream)
+                        t = bench.graph_time(torch, fn, stream, min_ms=1.0, reps=5)
                         inf = pl.info
                         cfg = {"h": ufi, "ufk": ufk, "T": inf["T"], "cta_warps": inf["cta_warps"],
                                "n_tiles": inf["n_tiles"], "n_heavy": inf["n_heavy"]}
