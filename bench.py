@@ -382,12 +382,14 @@ def run_escs(args):
     starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
+        torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx-include bench_timed/
         for s in range(args.steps):
             flush.zero_()
             torch.cuda._sleep(sleep_cycles)
             starts[s].record(stream)
             step()
             ends[s].record(stream)
+        torch.cuda.nvtx.range_pop()
         barrier()
         # ---- timed again with per-launch events (kernel durations for the roofline)
         pl_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]

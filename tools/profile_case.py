@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--config", default=None, help="c1/c4/c5 instead of a suite shape")
     ap.add_argument("--probe", action="store_true")
     ap.add_argument("--case", default=None, help="a problem name from bench.py's workloads")
+    ap.add_argument("--no-autotune", dest="autotune", action="store_false",
+                    help="plan with the parameter table (default: autotuned, as bench.py)")
     a = ap.parse_args()
     import torch
     from paper_2506_15174_b200 import escs, synth
@@ -37,12 +39,14 @@ def main():
         m, k = (int(x) for x in a.shape.split("x"))
         A = synth.magnitude_pruned(m, k, a.s, 1234)
         B = synth.dense_b(k, a.n, 99)
-    pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1])
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
+                           autotune=1 if a.autotune else 0)
     print(pl.info, flush=True)
     dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
     dC = torch.empty(A.m, B.shape[1], device="cuda")
     sink = torch.empty(pl.info["n_tiles"] * 32 * pl.info["cta_warps"], device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("profile_reps")      # ncu --nvtx-include profile_reps/
     for i in range(a.reps):
         torch.cuda._sleep(2_000_000)   # host runs ahead: events bracket the kernel only
         s.record()
@@ -53,6 +57,7 @@ def main():
         e.record()
         torch.cuda.synchronize()
         print(f"rep {i}: {s.elapsed_time(e) * 1e3:.1f} us", flush=True)
+    torch.cuda.nvtx.range_pop()
 
 
 if __name__ == "__main__":
