@@ -515,6 +515,8 @@ def run_escs(args):
         dom = int(np.argmax(per_prob))
         clocks = clk.summary()
         traffic, traffic_src = committed_traffic(args.workload) if world == 1 else (None, None)
+        n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+        gather_peak = n_sm * 64.0 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
@@ -534,6 +536,10 @@ def run_escs(args):
                          "kernel_ms_per_step": float(kern_ms.sum() / K),
                          "gather_GBps": gather,
                          "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)",
+                         "gather_roofline": {
+                             "achieved": gather, "unit": "GB/s",
+                             "peak": gather_peak, "frac": gather / gather_peak,
+                             "peak_source": "derived: SMs x 64 B/clk (L2->SM fill of a gathered row that misses L1; its L1 read doubles the 128 B/clk L1 data path) x max SM clock (MEASURED_PEAKS sm_max_mhz)"},
                          "attainable": None if probe_ms is None else {
                              "probe_ms_per_step": probe_ms / K,
                              "frac": probe_ms / float(kern_ms.sum()),
