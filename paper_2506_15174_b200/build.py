@@ -30,7 +30,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--ex
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function",
             "-I", os.path.join(CUDA, "include"), "-I", CSRC, "-I", os.path.join(ROOT, "include")]
 
-LIB_CU = ["launch.cu", "k_b32.cu", "k_b64.cu", "k_b128.cu", "k_b256.cu",
+LIB_CU = ["launch.cu", "k_b4.cu", "k_b8.cu", "k_b16.cu", "k_b32.cu", "k_b64.cu", "k_b128.cu", "k_b256.cu",
           "k_s1.cu", "k_s2.cu", "k_s4.cu", "k_s8.cu"]
 LIB_CPP = ["plan.cpp", "abi.cpp"]
 BENCH_CU = ["baselines.cu"]

@@ -236,7 +236,9 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16, variant 1..2)");
         return nullptr;
     }
-    if (p.variant == 1 && !(bCols == 32 || bCols == 64 || bCols == 128 || bCols == 256)) p.variant = 2;
+    if (p.variant == 1 && !(bCols == 4 || bCols == 8 || bCols == 16 || bCols == 32 || bCols == 64 ||
+                            bCols == 128 || bCols == 256))
+        p.variant = 2;
     if (!host_only && k >= (1 << 27)) {
         fail(ESCS_ERR_UNSUPPORTED, "device plans need k < 2^27 (packed column words)");
         return nullptr;
@@ -401,7 +403,7 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     if (!(ep && ep->ufk)) {
         const int U0 = best->params.ufk;
         for (int U : {4, 8}) {
-            if (U == U0) continue;
+            if (U == U0 || bCols < 32) continue;
             escs_params c = q;
             c.ufi = h;
             c.T = best->params.T;

@@ -8,6 +8,9 @@
 
 namespace escs {
 namespace kern {
+KernelFn get_b4(int, int, bool);
+KernelFn get_b8(int, int, bool);
+KernelFn get_b16(int, int, bool);
 KernelFn get_b32(int, int, bool);
 KernelFn get_b64(int, int, bool);
 KernelFn get_b128(int, int, bool);
@@ -35,6 +38,9 @@ namespace {
 kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
     if (vec) {
         switch (n) {
+            case 4: return kern::get_b4(h, ufk, probe);
+            case 8: return kern::get_b8(h, ufk, probe);
+            case 16: return kern::get_b16(h, ufk, probe);
             case 32: return kern::get_b32(h, ufk, probe);
             case 64: return kern::get_b64(h, ufk, probe);
             case 128: return kern::get_b128(h, ufk, probe);
@@ -43,6 +49,7 @@ kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
         }
     }
     if (probe) return nullptr;
+    if (ufk < 2) ufk = 2;   // the scalar map has UFk 2/4/8 instances
     if (n <= 32) return kern::get_s1(h, ufk, false);
     if (n <= 64) return kern::get_s2(h, ufk, false);
     if (n <= 128) return kern::get_s4(h, ufk, false);
@@ -99,7 +106,7 @@ bool kernel_supported(int h, int bcols, int variant, int ufk) {
 
 // floats per lane-column slot F of the lane map the launch will use
 static int lane_floats(int n, bool vec) {
-    if (vec) return n / 32;
+    if (vec) return n < 32 ? 4 : n / 32;   // bCols < 32: L = bCols/4 lanes x float4
     return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
 }
 

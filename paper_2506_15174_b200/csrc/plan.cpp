@@ -326,12 +326,14 @@ Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm)
     const double d = (double)nnz / ((double)m * (double)k);
     const double s = 1.0 - d;
     p.h = 1;
-    p.variant = (bcols == 32 || bcols == 64 || bcols == 128 || bcols == 256) ? 1 : 2;
+    p.variant = (bcols == 4 || bcols == 8 || bcols == 16 || bcols == 32 || bcols == 64 ||
+                 bcols == 128 || bcols == 256) ? 1 : 2;
     // more rows in flight per warp on the small, latency-bound layers; more
     // resident warps (fewer registers) on the large, L2-bandwidth-bound ones
     // (C4: 183 -> 135 us, C5: 2.63 -> 2.28 ms with UFk 4; profiles/r1_notes.md)
     const double g_est = (double)nnz;   // gcols at UFi = 1
     p.ufk = (bcols > 128 || g_est > 1.5e6) ? 4 : 8;
+    if (bcols < 32) p.ufk = bcols == 4 ? 1 : bcols == 8 ? 2 : 4;   // UFk x (32 / (bCols/4)) <= 32
     const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
     const double target_items = 1536.0 * (double)n_sm / 148.0;

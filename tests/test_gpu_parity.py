@@ -114,7 +114,7 @@ def test_empty_matrix_overwrites(torch_cuda):
         assert np.array_equal(C, np.zeros((37, n), np.float32))
 
 
-@pytest.mark.parametrize("n", [1, 4, 31, 33, 48, 96, 160, 200, 256])
+@pytest.mark.parametrize("n", [1, 4, 8, 16, 31, 33, 48, 96, 160, 200, 256])
 def test_bcols_tails_scalar_and_vector(torch_cuda, n):
     A0 = synth.random_csr(203, 150, 3000, n, empty_rows=(0, 5, 6, 7, 8), dense_rows=(100,))
     A, B = synth.dyadic_twin(A0, n, n + 1)
@@ -297,3 +297,13 @@ def test_autotuned_plan_parity(torch_cuda):
     C, _ = run_escs(torch_cuda, A, B, ufi=info["h"], T=info["T"], cta_warps=info["cta_warps"],
                     ufk=info["ufk"])
     check_exact(A, B, C)
+
+
+def test_dlmc_tall_shape(torch_cuda):
+    """DLMC's largest shape, 33,288 x 512, at 90% sparsity, bCols 64
+    and 4 (Fig. 10's narrow B): exact on the dyadic twin."""
+    A0 = synth.magnitude_pruned(33288, 512, 0.9, 33288)
+    for n in (64, 4):
+        A, B = synth.dyadic_twin(A0, n, n)
+        C, _ = run_escs(torch_cuda, A, B)
+        check_exact(A, B, C)
