@@ -306,10 +306,17 @@ def run_escs(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU (LOCAL_RANK); ESCS_BENCH_BACKEND=gloo lets a 1-GPU box
+    # exercise the N > 1 control flow with several ranks sharing the device
+    backend = os.environ.get("ESCS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2506_15174_b200 import escs, shard
 
