@@ -86,13 +86,22 @@ def test_suite_dyadic_exact(torch_cuda, shape, n):
 
 
 def test_transformer_suite_tolerance(torch_cuda):
+    """configs[1] in bench.py's launch configuration (autotuned plans)."""
     for p in synth.transformer_suite():
-        C, _ = run_escs(torch_cuda, p.A, p.B)
+        C, _ = run_escs(torch_cuda, p.A, p.B, autotune=1)
         check_tol(p.A, p.B, C)
 
 
 def test_resnet_suite_tolerance(torch_cuda):
+    """configs[2] in bench.py's launch configuration (autotuned plans)."""
     for p in synth.resnet_suite():
+        C, _ = run_escs(torch_cuda, p.A, p.B, autotune=1)
+        check_tol(p.A, p.B, C)
+
+
+def test_suite_default_plans_tolerance(torch_cuda):
+    """The parameter-table plans (escs_plan without autotuning) on both suites."""
+    for p in synth.suite(bcols=(64,)):
         C, _ = run_escs(torch_cuda, p.A, p.B)
         check_tol(p.A, p.B, C)
 
