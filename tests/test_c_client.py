@@ -1,0 +1,36 @@
+"""The C ABI is usable from plain C: tests/c/abi_client.c is compiled with gcc
+against include/escs.h and libescs.so and run (host-only part on CPU; the
+device part, with cudaMalloc'd buffers, on the GPU)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2506_15174_b200")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+
+
+@pytest.fixture(scope="module")
+def client(tmp_path_factory):
+    exe = str(tmp_path_factory.mktemp("c") / "abi_client")
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-o", exe,
+                           os.path.join(ROOT, "tests", "c", "abi_client.c"),
+                           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CUDA, "include"),
+                           "-L", PKG, "-lescs", "-Wl,-rpath," + PKG,
+                           "-L", os.path.join(CUDA, "lib64"), "-lcudart",
+                           "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
+    return exe
+
+
+def test_c_client_host(client):
+    r = subprocess.run([client], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "host ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_client_device(client):
+    r = subprocess.run([client, "device"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "device ok" in r.stdout
