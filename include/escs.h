@@ -123,6 +123,31 @@ int escs_pack(escs_plan_t plan, const float *vals, float *packed, void *stream);
 int escs_spmm_packed(escs_plan_t plan, const float *packed, const float *B, float *C,
                      void *stream);
 
+/*
+ * escs_spmm_scatter -- escs_spmm whose epilogue stores every output row i of
+ * the plan's A into each of the n_dst destination buffers at row
+ * row_offset + i (row-major, ld = bCols): with the destinations being the
+ * peers' C buffers of a row-block-sharded SpMM (mapped through CUDA IPC /
+ * symmetric memory over NVLink), this is the SpMM fused with the optional
+ * all-gather of C: each C tile crosses NVLink once, as it
+ * is produced, with no separate collective.  One launch; same contract as
+ * escs_spmm otherwise.
+ *   dsts        HOST array of n_dst DEVICE pointers (1 <= n_dst <= 8), each a
+ *               float[(row_offset + m) * bCols] buffer reachable from this
+ *               device (local or peer-mapped); not aliasing vals or B.
+ *   row_offset  first row of this plan's block in the destinations (>= 0).
+ *   flags       0, or ESCS_SCATTER_MULTICAST: n_dst must be 1 and dsts[0] an
+ *               NVLS multicast address (CUDA multicast object bound to every
+ *               rank's C); the epilogue then issues multimem.st, one store
+ *               per element reaching all GPUs through the NVSwitch.
+ * Errors: ESCS_ERR_ARG for NULL pointers, n_dst outside 1..8, negative
+ * row_offset, unknown flags or a device other than the plan's.
+ */
+#define ESCS_SCATTER_MULTICAST 1u
+int escs_spmm_scatter(escs_plan_t plan, const float *vals, const float *B,
+                      float *const *dsts, int32_t n_dst, int64_t row_offset, uint32_t flags,
+                      void *stream);
+
 /* Release the plan's host and device memory.  NULL is a no-op.  No call on
  * the plan may be in flight. */
 void escs_free(escs_plan_t plan);

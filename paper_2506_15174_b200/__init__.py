@@ -7,7 +7,7 @@ without the CUDA library; any compute call fails loudly if the library is
 missing.
 """
 __all__ = ["escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
-           "escs_plan_export", "escs_plan_info", "escs_pack", "escs_spmm_packed",
+           "escs_plan_export", "escs_plan_info", "escs_pack", "escs_spmm_packed", "escs_spmm_scatter",
            "escs_gather_probe", "Plan", "spmm", "synth", "shard"]
 
 

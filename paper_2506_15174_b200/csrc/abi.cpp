@@ -462,6 +462,34 @@ int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, voi
     return spmm_common(plan, vals, B, C, stream, false);
 }
 
+int escs_spmm_scatter(escs_plan_t plan, const float* vals, const float* B, float* const* dsts,
+                      int32_t n_dst, int64_t row_offset, uint32_t flags, void* stream) {
+    clear_error();
+    if (!plan || plan->host_only) return fail(ESCS_ERR_ARG, "plan is NULL or host-only");
+    if (!dsts || n_dst < 1 || n_dst > 8)
+        return fail(ESCS_ERR_ARG, "escs_spmm_scatter needs 1..8 destination buffers");
+    if (!B || (!vals && plan->host.header[3] > 0))
+        return fail(ESCS_ERR_ARG, "vals and B must be non-NULL device pointers");
+    if (row_offset < 0) return fail(ESCS_ERR_ARG, "row_offset must be >= 0");
+    if (flags & ~(uint32_t)ESCS_SCATTER_MULTICAST) return fail(ESCS_ERR_ARG, "unknown flags");
+    const bool mc = flags & ESCS_SCATTER_MULTICAST;
+    if (mc && n_dst != 1)
+        return fail(ESCS_ERR_ARG, "ESCS_SCATTER_MULTICAST takes exactly one (multicast) address");
+    bool vec_ok = aligned16(B);
+    for (int d = 0; d < n_dst; d++) {
+        if (!dsts[d]) return fail(ESCS_ERR_ARG, "NULL destination buffer");
+        vec_ok = vec_ok && aligned16(dsts[d]);
+    }
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev != plan->device)
+        return fail(ESCS_ERR_ARG, "current device differs from the plan's device");
+    int e = escs::launch_spmm(plan->dev, vals, B, nullptr, stream, vec_ok, false, dsts, n_dst,
+                              (long long)row_offset, mc);
+    if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
+                                          cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
 int escs_spmm_packed(escs_plan_t plan, const float* packed, const float* B, float* C,
                      void* stream) {
     return spmm_common(plan, packed, B, C, stream, true);

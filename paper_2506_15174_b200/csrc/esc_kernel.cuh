@@ -34,6 +34,7 @@ namespace kern {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kColBits = 27;                       // packed gcol: col | mask << 27
 constexpr int kColMask = (1 << kColBits) - 1;
+constexpr int kMaxScatter = 8;                     // escs_spmm_scatter destinations
 
 struct KParams {
     const int* __restrict__ gpk;       // packed gcols: column | pattern << 27
@@ -49,6 +50,12 @@ struct KParams {
     const float* __restrict__ B;
     float* __restrict__ C;
     int m, n;
+    // fused row-block all-gather (escs_spmm_scatter): every output row is
+    // also stored to extra[d] + (row_off + row) * n, d < n_extra -- the peers'
+    // C buffers (P2P / NVLink stores through mapped symmetric memory)
+    int n_extra, mc;                               // mc: extra[0] is a multicast address
+    long long row_off;
+    float* extra[kMaxScatter];
 };
 
 // L2 cache policies: the plan and value streams are read once per call
@@ -126,6 +133,23 @@ struct VecMap {
                     make_float4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
         }
     }
+    // Store through an NVLS multicast address (one store lands in every
+    // GPU's copy of C; escs_spmm_scatter with ESCS_SCATTER_MULTICAST).
+    __device__ static __forceinline__ void store_mc(float* row, const float (&a)[F], int, int lj) {
+        float* q = row + lj * F;
+        if constexpr (F == 1) {
+            asm volatile("multimem.st.weak.global.f32 [%0], %1;" :: "l"(q), "f"(a[0]) : "memory");
+        } else if constexpr (F == 2) {
+            asm volatile("multimem.st.weak.global.v2.f32 [%0], {%1,%2};"
+                         :: "l"(q), "f"(a[0]), "f"(a[1]) : "memory");
+        } else {
+#pragma unroll
+            for (int v = 0; v < F / 4; v++)
+                asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                             :: "l"(q + 4 * v), "f"(a[4 * v]), "f"(a[4 * v + 1]),
+                                "f"(a[4 * v + 2]), "f"(a[4 * v + 3]) : "memory");
+        }
+    }
 };
 
 // Scalar lane map (the paper's map(j, 32*WarpTile), Listings 5-6): lane owns
@@ -148,6 +172,15 @@ struct ScalarMap {
         for (int f = 0; f < F; f++) {
             const int j = lj + 32 * f;
             if (j < n) row[j] = a[f];
+        }
+    }
+    __device__ static __forceinline__ void store_mc(float* row, const float (&a)[F], int n, int lj) {
+#pragma unroll
+        for (int f = 0; f < F; f++) {
+            const int j = lj + 32 * f;
+            if (j < n)
+                asm volatile("multimem.st.weak.global.f32 [%0], %1;" :: "l"(row + j), "f"(a[f])
+                             : "memory");
         }
     }
 };
@@ -380,7 +413,14 @@ __device__ __forceinline__ void store_rows(const KParams& p, int panel, const fl
 #pragma unroll
     for (int r = 0; r < H; r++) {
         const int row = panel * H + r;
-        if ((r % Map::S) == sub && row < p.m) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
+        if ((r % Map::S) == sub && row < p.m) {
+            if (p.C) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
+            for (int d = 0; d < p.n_extra; d++) {   // fused all-gather epilogue
+                float* q = p.extra[d] + (size_t)(p.row_off + row) * p.n;
+                if (p.mc) Map::store_mc(q, a[r], p.n, lj);
+                else Map::store(q, a[r], p.n, lj);
+            }
+        }
     }
 }
 

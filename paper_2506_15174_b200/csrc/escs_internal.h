@@ -65,7 +65,8 @@ struct DevPlan {
 
 // Launch the ESC SpMM kernel (one launch).  Returns a cudaError_t value.
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
-                bool vec_ok, bool packed = false);
+                bool vec_ok, bool packed = false, float* const* extra = nullptr,
+                int n_extra = 0, long long row_off = 0, bool multicast = false);
 // escs_pack: packed[s] = vals[slot[s]].
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream);
 // Launch the gather probe (same walk, loads only).

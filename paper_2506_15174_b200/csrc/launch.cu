@@ -59,7 +59,7 @@ kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
 
 kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C,
                           bool packed = false) {
-    kern::KParams p;
+    kern::KParams p = {};
     p.packed = packed ? 1 : 0;
     p.gpk = dp.gpk;
     p.slot = dp.slot;
@@ -167,12 +167,17 @@ int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* strea
 }
 
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
-                bool vec_ok, bool packed) {
+                bool vec_ok, bool packed, float* const* extra, int n_extra, long long row_off,
+                bool multicast) {
     const bool vec = vec_ok && dp.variant == 1;
     kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, vals, B, C, packed);
+    p.n_extra = n_extra;
+    p.mc = multicast ? 1 : 0;
+    p.row_off = row_off;
+    for (int d = 0; d < n_extra && d < kern::kMaxScatter; d++) p.extra[d] = extra[d];
     return launch(fn, dp, p, smem_for(dp, vec), stream);
 }
 

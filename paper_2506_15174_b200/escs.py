@@ -22,7 +22,7 @@ PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "s
                "item_panel", "item_group_begin", "item_gcol_ptr")
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
                     "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
-                    "escs_pack", "escs_spmm_packed")
+                    "escs_pack", "escs_spmm_packed", "escs_spmm_scatter")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -61,6 +61,9 @@ _lib.escs_spmm.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.escs_spmm.restype = ctypes.c_int
 _lib.escs_spmm_packed.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.escs_spmm_packed.restype = ctypes.c_int
+_lib.escs_spmm_scatter.argtypes = [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i32, _i64,
+                                   ctypes.c_uint32, _vp]
+_lib.escs_spmm_scatter.restype = ctypes.c_int
 _lib.escs_pack.argtypes = [_vp, _vp, _vp, _vp]
 _lib.escs_pack.restype = ctypes.c_int
 _lib.escs_gather_probe.argtypes = [_vp, _vp, _vp, _vp]
@@ -197,6 +200,21 @@ def escs_pack(plan: Plan, vals, packed, stream=None) -> None:
 def escs_spmm_packed(plan: Plan, packed, B, C, stream=None) -> None:
     """C = A x B with values pre-packed by escs_pack."""
     rc = _lib.escs_spmm_packed(plan.handle, _ptr(packed), _ptr(B), _ptr(C), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+ESCS_SCATTER_MULTICAST = 1
+
+
+def escs_spmm_scatter(plan: Plan, vals, B, dsts, row_offset: int, stream=None,
+                      multicast: bool = False) -> None:
+    """Store C = A x B into every buffer of `dsts` (device tensors or raw
+    pointers, e.g. the peers' symmetric-memory C) at rows row_offset + i;
+    multicast=True: dsts is one NVLS multicast address."""
+    arr = (ctypes.c_void_p * len(dsts))(*[_ptr(d) for d in dsts])
+    rc = _lib.escs_spmm_scatter(plan.handle, _ptr(vals), _ptr(B), arr, len(dsts), int(row_offset),
+                                ESCS_SCATTER_MULTICAST if multicast else 0, _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
 

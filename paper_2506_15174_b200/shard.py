@@ -81,3 +81,47 @@ def sum_over_ranks(values, device=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return [float(x) for x in t.tolist()]
+
+
+class FusedGather:
+    """Full m x n C in symmetric memory on every rank, for the SpMM fused
+    with its all-gather (SURVEY §8(e) "optional NCCL all-gather of C", NEXT
+    row f1): rank r's escs kernel stores each finished C row straight into
+    every rank's C over NVLink (peer pointers, or one NVLS multicast store
+    when the switch supports it), so there is no separate collective and the
+    transfer overlaps the SpMM tile by tile.
+
+    run() = symmetric-memory barrier (peers are done reading the previous C)
+    -> escs_spmm_scatter -> barrier (all rows landed).  Plumbing only."""
+
+    def __init__(self, m: int, n: int, group=None, multicast: bool = True):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.m, self.n = m, n
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.C = symm.empty((m, n), dtype=torch.float32, device=dev)
+        self.handle = symm.rendezvous(self.C, self.group)
+        off = self.C.storage_offset()
+        self.peers = [self.handle.get_buffer(r, (m, n), torch.float32, off)
+                      for r in range(self.world)]
+        self.mc_ptr = None
+        if multicast and self.world > 1 and self.handle.has_multicast_support():
+            self.mc_ptr = self.handle.multicast_ptr + 4 * off
+        self.r0, self.r1 = shard_rows(m, self.world, self.rank)
+
+    @property
+    def mode(self) -> str:
+        return "multicast" if self.mc_ptr is not None else "p2p"
+
+    def run(self, plan, vals, B, stream=None) -> None:
+        from . import escs
+        self.handle.barrier(channel=0)
+        if self.mc_ptr is not None:
+            escs.escs_spmm_scatter(plan, vals, B, [self.mc_ptr], self.r0, stream, multicast=True)
+        else:
+            escs.escs_spmm_scatter(plan, vals, B, self.peers, self.r0, stream)
+        self.handle.barrier(channel=0)

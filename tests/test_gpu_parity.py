@@ -316,3 +316,54 @@ def test_dlmc_tall_shape(torch_cuda):
         A, B = synth.dyadic_twin(A0, n, n)
         C, _ = run_escs(torch_cuda, A, B)
         check_exact(A, B, C)
+
+
+def test_scatter_epilogue_multiple_destinations(torch_cuda):
+    """escs_spmm_scatter (fused all-gather epilogue, NEXT row f1): row-block
+    shards of A each store their C rows into 3 full-size destination buffers
+    at their row offset; every destination must equal the unsharded oracle
+    result exactly (dyadic twin), for vector and scalar lane maps."""
+    torch = torch_cuda
+    from paper_2506_15174_b200 import escs
+    A0 = synth.magnitude_pruned(1000, 700, 0.8, 31)
+    for n in (128, 48):
+        A, B = synth.dyadic_twin(A0, n, 32)
+        dB = torch.from_numpy(B).cuda()
+        dsts = [torch.full((A.m, n), float("nan"), device="cuda") for _ in range(3)]
+        for r in range(3):
+            r0, r1 = synth.shard_bounds(A.m, 3, r)
+            S = synth.row_block(A, r0, r1)
+            pl = escs.escs_plan(S.m, S.k, S.nnz, S.rowptr, S.colidx, n)
+            escs.escs_spmm_scatter(pl, torch.from_numpy(S.vals).cuda(), dB, dsts, r0)
+        torch.cuda.synchronize()
+        ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B)
+        for d in dsts:
+            assert np.array_equal(d.cpu().numpy().astype(np.float64), ref)
+    with pytest.raises(escs.EscsError):
+        escs.escs_spmm_scatter(pl, torch.from_numpy(S.vals).cuda(), dB, dsts * 3, 0)
+
+
+def test_fused_gather_symmetric_memory_world1(torch_cuda):
+    """FusedGather over torch symmetric memory on a 1-rank NCCL group: the
+    rendezvous, peer-buffer mapping, barriers and scatter launch of the N > 1
+    fused path, checked against the oracle (one GPU is all a test box has)."""
+    torch = torch_cuda
+    import os
+    import torch.distributed as dist
+    from paper_2506_15174_b200 import escs, shard
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        fg = shard.FusedGather(777, 64)
+    except Exception as e:                      # symmetric memory not usable here
+        pytest.skip(f"symmetric memory unavailable: {e}")
+    A0 = synth.magnitude_pruned(777, 300, 0.9, 41)
+    A, B = synth.dyadic_twin(A0, 64, 42)
+    pl = escs.escs_plan(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64)
+    fg.C.fill_(float("nan"))
+    fg.run(pl, torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda())
+    torch.cuda.synchronize()
+    ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B)
+    assert np.array_equal(fg.C.cpu().numpy().astype(np.float64), ref)
