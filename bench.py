@@ -428,8 +428,9 @@ def run_escs(args):
     # ---- e2e: host buffers through the public API, copies inside the timed region.
     # The step's inputs (every layer's values and B) sit in one pinned host
     # buffer and its outputs land in one pinned host buffer; the step is cut
-    # into 4 chunks of layers pipelined over two streams (H2D of chunk j+1
-    # overlaps the SpMMs of chunk j; D2H of chunk j follows its SpMMs).
+    # into --e2e-chunks chunks of layers pipelined over three streams (H2D of
+    # chunk j+1 overlaps the SpMMs of chunk j; D2H of chunk j follows its
+    # SpMMs on its own stream, overlapping later H2D and SpMMs).
     sizes_in = [(d["A"].nnz, p.B.size) for p, d in shard_problems]
     off_in, tot_in = [], 0
     for nv, nb in sizes_in:
@@ -449,9 +450,14 @@ def run_escs(args):
         h_in[off_in[i] + vpad[i]:off_in[i] + vpad[i] + nb] = torch.from_numpy(p.B.ravel())
     d_in = torch.empty(tot_in, dtype=torch.float32, device=device)
     d_out = torch.empty(tot_out, dtype=torch.float32, device=device)
-    nchunk = min(4, nprob)
-    bounds = [(c * nprob) // nchunk for c in range(nchunk + 1)]
+    nchunk = min(args.e2e_chunks, nprob)
+    # chunk bounds balanced by input bytes (layer sizes differ by ~50x)
+    cuts = sorted({min(nprob - 1, int(np.searchsorted(off_in, c * tot_in / nchunk)))
+                   for c in range(1, nchunk)} - {0})
+    bounds = [0] + cuts + [nprob]
+    nchunk = len(bounds) - 1
     copy_s = torch.cuda.Stream(device)
+    out_s = torch.cuda.Stream(device)
     h2d = 4 * tot_in
     d2h = 4 * tot_out
 
@@ -477,7 +483,10 @@ def run_escs(args):
                 Cv = d_out[off_out[i]:off_out[i] + d["C"].numel()]
                 escs.escs_spmm(d["plan"], v, Bv, Cv, stream)
             lo, hi = off_out[a], (off_out[b] if b < nprob else tot_out)
-            h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
+            out_s.wait_stream(stream)
+            with torch.cuda.stream(out_s):         # D2H on its own engine/stream
+                h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
+        stream.wait_stream(out_s)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
@@ -491,6 +500,21 @@ def run_escs(args):
         ee[s].record(stream)
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
+    # the copies alone (same buffers, same chunking): the PCIe floor of e2e
+    ca, cb = ev(), ev()
+    ca.record(stream)
+    for _ in range(args.steps):
+        with torch.cuda.stream(copy_s):
+            copy_s.wait_stream(stream)
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(out_s):
+            out_s.wait_stream(stream)
+            h_out.copy_(d_out, non_blocking=True)
+        stream.wait_stream(copy_s)
+        stream.wait_stream(out_s)
+    cb.record(stream)
+    torch.cuda.synchronize(device)
+    copy_ms = ca.elapsed_time(cb) / args.steps
 
     # ---- optional all-gather of C (NCCL), timed separately (not on the hot path)
     allgather_ms = None
@@ -503,6 +527,34 @@ def run_escs(args):
         gb.record(stream)
         barrier()
         allgather_ms = shard.max_over_ranks([ga.elapsed_time(gb)], device)[0]
+    # ---- SpMM fused with the all-gather (NEXT f1): escs_spmm_scatter stores
+    # each C row into every rank's symmetric-memory C (NVLink P2P / NVLS
+    # multicast); timed per step against SpMM + NCCL all-gather
+    fused = None
+    if world > 1 and args.allgather and mode == "rows" and backend == "nccl":
+        try:
+            fgs = [shard.FusedGather(p.A.m, p.bcols) for p, _ in shard_problems]
+            def fused_step():
+                for fg, (p, d) in zip(fgs, shard_problems):
+                    fg.run(d["plan"], d["vals"], d["B"], stream)
+            def split_step():
+                for p, d in shard_problems:
+                    escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
+                    shard.all_gather_rows(d["C"], p.A.m, world)
+            fused = {"mode": fgs[0].mode}
+            for name, fn in (("fused_ms_per_step", fused_step), ("spmm_then_nccl_ms_per_step", split_step)):
+                for _ in range(args.warmup):
+                    fn()
+                fa, fb = ev(), ev()
+                barrier()
+                fa.record(stream)
+                for _ in range(args.steps):
+                    fn()
+                fb.record(stream)
+                barrier()
+                fused[name] = shard.max_over_ranks([fa.elapsed_time(fb) / args.steps], device)[0]
+        except Exception as e:            # symmetric memory unavailable on this box
+            fused = {"unavailable": str(e)[:200]}
 
     # ---- reduce over ranks: flops SUM, times MAX
     my_flops = sum(d["flops"] for _, d in shard_problems)
@@ -554,11 +606,17 @@ def run_escs(args):
             "gpu_launches": nprob * K,   # this rank's escs_spmm launches in the timed region
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "copies_only_ms_per_step": copy_ms,
+                    "copy_floor": (f"{(h2d + d2h) / (copy_ms * 1e-3) / 1e9:.1f} GB/s host<->device "
+                                   f"(H2D and D2H concurrent); e2e is {e2e_ms / K / copy_ms:.2f}x "
+                                   "the copies alone")},
             "plan_seconds": plan_s,
         }
         if allgather_ms is not None:
             result["allgather_ms_per_step"] = allgather_ms
+        if fused is not None:
+            result["fused_allgather"] = fused
         if world == 1 and not args.no_cpu:
             v, reps, secs, thr = oracle_time(problems, budget_s=args.cpu_budget)
             result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
@@ -592,6 +650,8 @@ def main(argv=None):
                     help="plan with the parameter table only (default: plan-time autotuning)")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],
                     help="N>1: partition a suite by problems or row-block shard every problem")
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="e2e: copy/compute pipeline depth (chunks of layers per step)")
     ap.add_argument("--allgather", action="store_true",
                     help="N>1: also time the optional NCCL all-gather of C (not on the hot path)")
     args = ap.parse_args(argv)
