@@ -76,6 +76,8 @@ def workload(name):
         return synth.resnet_suite(), "configs[2]: ResNet-50 im2col 256x2304/512x4608/2048x512 x 70-98% x bCols 32/64/128"
     if name == "suite":
         return synth.suite(), "configs[1]+[2]: Transformer + ResNet-50 suites x bCols 32/64/128"
+    if name == "wide":
+        return synth.suite(bcols=(256,)), "suites at bCols 256 (beyond the north_star range; tuning only)"
     if name in ("c1", "c4", "c5"):
         p = synth.config(name)
         return [p], p.name
@@ -236,6 +238,36 @@ def graph_time(torch, fn, stream, min_ms=2.0, reps=11):
     return statistics.median(ts)
 
 
+def gather_ceiling(torch, dev, stream, n_sm):
+    """Measured B-row gather ceiling (GB/s): bl_gather_peak gathers pseudo-
+    random 512-byte rows of a 64 MiB L2-resident B (C5's B) with no index
+    loads, values or FMAs; best of 6 lane maps / depths, 64 warps per SM."""
+    import ctypes
+    from paper_2506_15174_b200.build import BENCH_LIB
+    bl = ctypes.CDLL(BENCH_LIB)
+    bl.bl_gather_peak.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
+    k = 131072
+    B = torch.rand(k, 128, device=dev)
+    sink = torch.zeros(256, device=dev)
+    ctas, rpw = n_sm * 8, 2048
+    rows = ctas * 8 * rpw
+    best = None
+    for v in range(6):
+        for _ in range(2):
+            assert bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream) == 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream)
+        b.record(stream)
+        b.synchronize()
+        gbs = 3 * rows * 512 / (a.elapsed_time(b) * 1e-3) / 1e9
+        best = gbs if best is None else max(best, gbs)
+    del B
+    return best
+
+
 def compare_baselines(torch, problems, dev, stream):
     """Per-case hot-L2 times for escs, cuSPARSE (best of 4 algorithms),
     cuBLAS fp32 and cuBLAS TF32 (context), same inputs, same protocol."""
@@ -281,7 +313,7 @@ def compare_baselines(torch, problems, dev, stream):
         del Ad
         inf = d["plan"].info
         rows.append({"case": p.name, "escs_us": 1e3 * t_escs,
-                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "n_tiles", "n_heavy", "G")},
+                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")},
                      "cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
                      "cublas_us": 1e3 * t_cublas, "cublas_tf32_us": 1e3 * t_tf32,
                      "gflops_escs": p.flops / (t_escs * 1e-3) / 1e9})
@@ -569,13 +601,20 @@ def run_escs(args):
         value = flops_all * K / (total_ms * 1e-3) / 1e9
         # roofline of the (only) kernel: compulsory bytes per launch / launch duration
         achieved = my_bytes * K / (kern_ms.sum() * 1e-3) / 1e9
-        gather = sum(d["gather_bytes"] for _, d in shard_problems) * K / (kern_ms.sum() * 1e-3) / 1e9
+        gather = sum(d["gather_bytes"] for _, d in shard_problems) * K / (total_ms * 1e-3) / 1e9
         per_prob = kern_ms.mean(axis=0)
         dom = int(np.argmax(per_prob))
         clocks = clk.summary()
         traffic, traffic_src = committed_traffic(args.workload) if world == 1 else (None, None)
         n_sm = torch.cuda.get_device_properties(device).multi_processor_count
-        gather_peak = n_sm * 64.0 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        gather_derived = n_sm * 64.0 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
+        try:
+            gather_peak, gather_src = gather_ceiling(torch, device, stream, n_sm), (
+                "measured in this run: bl_gather_peak (libescs_bench.so) gathers pseudo-random 512-byte "
+                "rows of a 64 MiB L2-resident B, no index loads / values / FMAs, best of 6 lane maps")
+        except (OSError, AssertionError):
+            gather_peak, gather_src = gather_derived, "derived: SMs x 64 B/clk x max SM clock"
+        step_bytes_per_s = my_bytes * K / (total_ms * 1e-3) / 1e9
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
@@ -584,9 +623,13 @@ def run_escs(args):
                        "l2": "flushed before every step (256 MiB write); each problem touched once per step",
                        "plans": ("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates)"
                                  if args.autotune else "parameter table (escs_plan defaults)"),
-                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "variant")}},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
+                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}},
+            "roofline": {"bound": "hbm", "achieved": step_bytes_per_s, "peak": hbm, "unit": "GB/s",
+                         "frac": step_bytes_per_s / hbm, "traffic": traffic,
+                         "achieved_how": ("algorithmic bytes of the step / timed step (CUDA events on the "
+                                          "launching stream; the timed region holds only escs_spmm launches, "
+                                          "back to back with PDL)"),
+                         "achieved_per_launch_bracketed": achieved,
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": my_bytes / nprob,
                          "peak_source": peak_src,
@@ -598,7 +641,8 @@ def run_escs(args):
                          "gather_roofline": {
                              "achieved": gather, "unit": "GB/s",
                              "peak": gather_peak, "frac": gather / gather_peak,
-                             "peak_source": "derived: SMs x 64 B/clk (L2->SM fill of a gathered row that misses L1; its L1 read doubles the 128 B/clk L1 data path) x max SM clock (MEASURED_PEAKS sm_max_mhz)"},
+                             "peak_source": gather_src,
+                             "derived_64B_per_clk": gather_derived},
                          "attainable": None if probe_ms is None else {
                              "probe_ms_per_step": probe_ms / K,
                              "frac": probe_ms / float(kern_ms.sum()),

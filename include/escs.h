@@ -177,7 +177,12 @@ typedef struct {
                              Adds a few ms to escs_plan; the plan arrays are
                              still the canonical plan of the chosen (UFi, T).
                              Also enabled by ESCS_AUTOTUNE=1.                  */
-    int32_t reserved[4];  /* must be zero                                        */
+    int32_t colf;         /* B columns per lane of the vector kernel: the bCols
+                             coarsening factor (register tile of B columns,
+                             §3.4).  0 = default (4; 8 at bCols 256); 8 or 16
+                             at bCols 32..256 (UFi = 1 only).  Searched by the
+                             autotuner when 0.                                  */
+    int32_t reserved[3];  /* must be zero                                        */
 } escs_params;
 
 /* escs_plan with explicit parameters; p may be NULL (= all auto). */
@@ -218,6 +223,7 @@ typedef struct {
     double plan_seconds;    /* host enumeration time                              */
     int32_t ctas_per_sm;    /* resident CTAs per SM of the launch (occupancy), 0 host-only */
     int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing */
+    int32_t colf;           /* B columns per lane of the launch's lane map (0 scalar map) */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);

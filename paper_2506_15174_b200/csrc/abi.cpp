@@ -46,7 +46,7 @@ int sm_count_of_current_device() {
     return n > 0 ? n : 148;
 }
 
-// ESCS_PARAMS="ufi=4,T=64,warps=8,variant=1,ufk=4"
+// ESCS_PARAMS="ufi=4,T=64,warps=8,variant=1,ufk=4,colf=8"
 void apply_env(escs::Params& p, bool& set_warps) {
     const char* e = std::getenv("ESCS_PARAMS");
     if (!e) return;
@@ -65,6 +65,7 @@ void apply_env(escs::Params& p, bool& set_warps) {
             else if (k == "warps") { p.cta_warps = v; set_warps = true; }
             else if (k == "variant") p.variant = v;
             else if (k == "ufk") p.ufk = v;
+            else if (k == "colf") p.colf = v;
         }
         i = j + 1;
     }
@@ -200,7 +201,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         return nullptr;
     }
     if (ep) {
-        for (int i = 0; i < 4; i++)
+        for (int i = 0; i < 3; i++)
             if (ep->reserved[i] != 0) {
                 fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
                 return nullptr;
@@ -229,6 +230,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         if (ep->cta_warps) { p.cta_warps = ep->cta_warps; set_warps = true; }
         if (ep->variant) p.variant = ep->variant;
         if (ep->ufk) p.ufk = ep->ufk;
+        if (ep->colf) p.colf = ep->colf;
         if (ep->nthreads) p.nthreads = ep->nthreads;
     }
     if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > 16)) ||
@@ -243,10 +245,17 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         fail(ESCS_ERR_UNSUPPORTED, "device plans need k < 2^27 (packed column words)");
         return nullptr;
     }
-    if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk)) {
+    if (p.variant != 1) p.colf = 0;
+    else if (p.colf == 0) p.colf = escs::default_colf(bCols);
+    // automatic UFk: fall back to the largest UFk the chosen lane map has
+    // (wide per-lane tiles carry fewer rows in flight: UFk x colf <= 64)
+    if (!host_only && !(ep && ep->ufk) && !std::getenv("ESCS_PARAMS"))
+        while (p.ufk > 1 && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf)) p.ufk /= 2;
+    if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf)) {
         fail(ESCS_ERR_UNSUPPORTED, "no kernel for ufi=" + std::to_string(p.h) + " bCols=" +
                                        std::to_string(bCols) + " variant=" +
-                                       std::to_string(p.variant) + " ufk=" + std::to_string(p.ufk));
+                                       std::to_string(p.variant) + " ufk=" + std::to_string(p.ufk) +
+                                       " colf=" + std::to_string(p.colf));
         return nullptr;
     }
     escs_plan_impl* P = new (std::nothrow) escs_plan_impl();
@@ -273,7 +282,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     auto& dp = P->dev;
     dp.m = (int)m; dp.k = (int)k; dp.nnz = (int)nnz; dp.bcols = bCols; dp.h = p.h;
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
-    dp.ufk = p.ufk; dp.any_sync = P->host.any_sync;
+    dp.ufk = p.ufk; dp.colf = p.colf; dp.any_sync = P->host.any_sync;
     {
         const char* e = std::getenv("ESCS_PDL");
         dp.pdl = !(e && e[0] == '0');
@@ -410,6 +419,25 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             c.cta_warps = best->params.cta_warps;
             c.ufk = U;
             consider(c);
+        }
+    }
+    // stage 4: B columns per lane (bCols coarsening of the vector lane map;
+    // wider per-lane tiles trade shuffles per gathered row for fewer lanes)
+    if (!(ep && ep->colf) && best->params.h == 1 && best->dev.variant == 1) {
+        const int F0 = best->params.colf;
+        for (int F : {4, 8, 16}) {
+            if (F == F0) continue;
+            for (int U : {best->params.ufk, 4, 2}) {
+                escs_params c = q;
+                c.ufi = 1;
+                c.T = best->params.T;
+                c.cta_warps = best->params.cta_warps;
+                c.ufk = U;
+                c.colf = F;
+                if (!escs::kernel_supported(1, bCols, 1, U, F)) continue;
+                consider(c);
+                break;
+            }
         }
     }
     best->autotuned = true;
@@ -571,6 +599,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->plan_seconds = h.plan_seconds;
     o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false);
     o->autotuned = plan->autotuned ? 1 : 0;
+    o->colf = plan->dev.variant == 1 ? plan->params.colf : 0;
     return ESCS_OK;
 }
 

@@ -17,7 +17,57 @@ struct BlSparse {
     cusparseSpMMAlg_t alg = CUSPARSE_SPMM_ALG_DEFAULT;
 };
 
+// Gather ceiling (bench roofline): warps gather pseudo-random 512-byte rows
+// (bCols 128, fp32) of an L2-resident B with no index loads, no values and
+// no FMAs -- the most B-row bytes per second the SM memory pipeline delivers
+// to registers for this access pattern.  L lanes per row, 16 B per lane per
+// load instruction (interleaved), U rows in flight per sub-warp.
+template <int L, int U>
+__global__ void __launch_bounds__(256) gather_peak_kernel(const float4* __restrict__ B, int k,
+                                                          long long rows_per_warp,
+                                                          float* __restrict__ sink) {
+    constexpr int F4 = 32 / L, S = 32 / L;   // float4 per lane per row; rows per instruction
+    const int lane = threadIdx.x & 31, sub = lane / L, lj = lane % L;
+    const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long i = 0; i < rows_per_warp; i += S * U) {
+        float4 b[U][F4];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const unsigned r = (unsigned)((w * rows_per_warp + i + u * S + sub) * 2654435761ull) % (unsigned)k;
+#pragma unroll
+            for (int v = 0; v < F4; v++) b[u][v] = __ldg(B + (size_t)r * 32 + v * L + lj);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+            for (int v = 0; v < F4; v++) {
+                acc.x += b[u][v].x; acc.y += b[u][v].y; acc.z += b[u][v].z; acc.w += b[u][v].w;
+            }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1234.5f) sink[threadIdx.x] = acc.x;   // keep the loads live
+}
+
 extern "C" {
+
+// One launch of the gather ceiling kernel: `variant` 0..5 picks (L, U) in
+// {32,16,8} x {4,8}; grid = ctas x 256 threads; rows_per_warp rows each.
+int bl_gather_peak(const float* B, int k, int variant, int ctas, long long rows_per_warp,
+                   float* sink, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const float4* B4 = reinterpret_cast<const float4*>(B);
+    switch (variant) {
+        case 0: gather_peak_kernel<32, 4><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        case 1: gather_peak_kernel<32, 8><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        case 2: gather_peak_kernel<16, 4><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        case 3: gather_peak_kernel<16, 8><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        case 4: gather_peak_kernel<8, 4><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        case 5: gather_peak_kernel<8, 8><<<ctas, 256, 0, st>>>(B4, k, rows_per_warp, sink); break;
+        default: return -1;
+    }
+    return (int)cudaGetLastError();
+}
+
 
 // alg: 0 = DEFAULT, 1 = CSR_ALG1, 2 = CSR_ALG2, 3 = CSR_ALG3.  Row-major B/C.
 // Returns NULL if this algorithm rejects the configuration.

@@ -34,7 +34,10 @@ namespace kern {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kColBits = 27;                       // packed gcol: col | mask << 27
 constexpr int kColMask = (1 << kColBits) - 1;
-constexpr int kMaxScatter = 8;                     // escs_spmm_scatter destinations
+constexpr int kMaxScatter = 8;
+#ifndef ESC_MINB
+#define ESC_MINB 1   // min resident 512-thread blocks per SM in __launch_bounds__
+#endif                     // escs_spmm_scatter destinations
 
 struct KParams {
     const int* __restrict__ gpk;       // packed gcols: column | pattern << 27
@@ -117,9 +120,14 @@ template <int L_, int F_>
 struct VecMap {
     static constexpr int L = L_, F = F_, S = 32 / L_;
     static constexpr bool kVec = true;
-    __device__ static __forceinline__ int col(int lj, int f) { return lj * F + f; }
+    // F > 4: float4 v of lane lj sits at column (v*L + lj)*4, so each 128-bit
+    // load instruction of the L lanes reads one contiguous L*16-byte span (one
+    // L1 wavefront per 128-byte line, no strided replays)
+    __device__ static __forceinline__ int col(int lj, int f) {
+        return F <= 4 ? lj * F + f : (((f >> 2) * L + lj) << 2) + (f & 3);
+    }
     __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lj) {
-        const float* q = row + lj * F;
+        const float* q = row + (F <= 4 ? lj * F : 4 * lj);
         const unsigned long long pol = policy_last();
         if constexpr (F == 1) {
             asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
@@ -133,11 +141,11 @@ struct VecMap {
                 asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                              : "=f"(b[4 * v]), "=f"(b[4 * v + 1]), "=f"(b[4 * v + 2]),
                                "=f"(b[4 * v + 3])
-                             : "l"(q + 4 * v), "l"(pol));
+                             : "l"(q + 4 * v * L), "l"(pol));
         }
     }
     __device__ static __forceinline__ void store(float* row, const float (&a)[F], int, int lj) {
-        float* q = row + lj * F;
+        float* q = row + (F <= 4 ? lj * F : 4 * lj);
         if constexpr (F == 1) {
             q[0] = a[0];
         } else if constexpr (F == 2) {
@@ -145,14 +153,14 @@ struct VecMap {
         } else {
 #pragma unroll
             for (int v = 0; v < F / 4; v++)
-                reinterpret_cast<float4*>(q)[v] =
+                *reinterpret_cast<float4*>(q + 4 * v * L) =
                     make_float4(a[4 * v], a[4 * v + 1], a[4 * v + 2], a[4 * v + 3]);
         }
     }
     // Store through an NVLS multicast address (one store lands in every
     // GPU's copy of C; escs_spmm_scatter with ESCS_SCATTER_MULTICAST).
     __device__ static __forceinline__ void store_mc(float* row, const float (&a)[F], int, int lj) {
-        float* q = row + lj * F;
+        float* q = row + (F <= 4 ? lj * F : 4 * lj);
         if constexpr (F == 1) {
             asm volatile("multimem.st.weak.global.f32 [%0], %1;" :: "l"(q), "f"(a[0]) : "memory");
         } else if constexpr (F == 2) {
@@ -162,7 +170,7 @@ struct VecMap {
 #pragma unroll
             for (int v = 0; v < F / 4; v++)
                 asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};"
-                             :: "l"(q + 4 * v), "f"(a[4 * v]), "f"(a[4 * v + 1]),
+                             :: "l"(q + 4 * v * L), "f"(a[4 * v]), "f"(a[4 * v + 1]),
                                 "f"(a[4 * v + 2]), "f"(a[4 * v + 3]) : "memory");
         }
     }
@@ -583,7 +591,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
 // dynamically, and the counter atomics and extra barriers cost 0.2-1.5 us per
 // launch on the latency-bound suite -- profiles/r1_notes.md.)
 template <int H, class Map, int U, bool PROBE>
-__global__ void __launch_bounds__(512, 1) esc_spmm_kernel(KParams p) {
+__global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_kernel(KParams p) {
     extern __shared__ __align__(16) float smem[];
     grid_dep_launch();   // the next launch may start reading its plan
     process_tile<H, Map, U, PROBE>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31);

@@ -14,6 +14,7 @@ struct Params {
     int cta_warps = 8;  // warps per CTA tile
     int variant = 1;    // 1 = vector (float4) lane map, 2 = scalar lane map
     int ufk = 4;        // B-row loads in flight per sub-warp step (UFk)
+    int colf = 0;       // B columns per lane of the vector map (bCols coarsening), 0 = default
     int nthreads = 0;   // planner threads
 };
 
@@ -58,7 +59,7 @@ struct DevPlan {
     const int32_t* heavy = nullptr;     // int4[n_heavy]
     float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
     int32_t* counters = nullptr;        // int32[n_heavy]
-    int m = 0, k = 0, nnz = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4;
+    int m = 0, k = 0, nnz = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4, colf = 0;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
 };
@@ -74,7 +75,8 @@ int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, b
 // Prepare kernel attributes (dynamic smem limits) once per plan.
 int prepare_kernels(DevPlan& dp);
 // Does a kernel instance exist for this configuration?
-bool kernel_supported(int h, int bcols, int variant, int ufk);
+bool kernel_supported(int h, int bcols, int variant, int ufk, int colf);
+int default_colf(int bcols);
 size_t smem_bytes(const DevPlan& dp);
 // Resident CTAs per SM for this plan's launch configuration.
 int blocks_per_sm(const DevPlan& dp, bool vec, bool probe);

@@ -5,21 +5,9 @@
 
 #include "esc_kernel.cuh"
 #include "escs_internal.h"
+#include "k_table.h"
 
 namespace escs {
-namespace kern {
-KernelFn get_b4(int, int, bool);
-KernelFn get_b8(int, int, bool);
-KernelFn get_b16(int, int, bool);
-KernelFn get_b32(int, int, bool);
-KernelFn get_b64(int, int, bool);
-KernelFn get_b128(int, int, bool);
-KernelFn get_b256(int, int, bool);
-KernelFn get_s1(int, int, bool);
-KernelFn get_s2(int, int, bool);
-KernelFn get_s4(int, int, bool);
-KernelFn get_s8(int, int, bool);
-}  // namespace kern
 
 namespace kern {
 // escs_pack: packed[s] = vals[slot[s]] (the paper's ANNZ, §3.3.3).
@@ -35,19 +23,8 @@ __global__ void __launch_bounds__(256) esc_pack_kernel(const int* __restrict__ s
 
 namespace {
 
-kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe) {
-    if (vec) {
-        switch (n) {
-            case 4: return kern::get_b4(h, ufk, probe);
-            case 8: return kern::get_b8(h, ufk, probe);
-            case 16: return kern::get_b16(h, ufk, probe);
-            case 32: return kern::get_b32(h, ufk, probe);
-            case 64: return kern::get_b64(h, ufk, probe);
-            case 128: return kern::get_b128(h, ufk, probe);
-            case 256: return kern::get_b256(h, ufk, probe);
-            default: return nullptr;
-        }
-    }
+kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe, int colf) {
+    if (vec) return kern::get_vec(n, colf > 0 ? colf : kern::default_colf(n), h, ufk, probe);
     if (probe) return nullptr;
     if (ufk < 2) ufk = 2;   // the scalar map has UFk 2/4/8 instances
     if (n <= 32) return kern::get_s1(h, ufk, false);
@@ -98,10 +75,12 @@ int launch(kern::KernelFn fn, const DevPlan& dp, const kern::KParams& p, size_t 
 
 }  // namespace
 
-bool kernel_supported(int h, int bcols, int variant, int ufk) {
+int default_colf(int bcols) { return kern::default_colf(bcols); }
+
+bool kernel_supported(int h, int bcols, int variant, int ufk, int colf) {
     if (h < 1 || h > 4 || bcols < 1 || bcols > 256) return false;
-    return select_kernel(h, bcols, variant == 1, ufk, false) != nullptr &&
-           select_kernel(h, bcols, false, ufk, false) != nullptr;
+    return select_kernel(h, bcols, variant == 1, ufk, false, colf) != nullptr &&
+           select_kernel(h, bcols, false, ufk, false, 0) != nullptr;
 }
 
 // floats per lane-column slot F of the lane map the launch will use
@@ -127,7 +106,7 @@ int prepare_kernels(DevPlan& dp) {
         if (vec && dp.variant != 1) continue;
         const size_t smem = smem_for(dp, vec == 1);
         if (smem <= 48 * 1024) continue;
-        kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec == 1, dp.ufk, false);
+        kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec == 1, dp.ufk, false, vec ? dp.colf : 0);
         if (!fn) continue;
         cudaFuncAttributes attr;
         cudaError_t e = cudaFuncGetAttributes(&attr, (const void*)fn);
@@ -137,7 +116,7 @@ int prepare_kernels(DevPlan& dp) {
                                  (int)smem);
         if (e != cudaSuccess) return (int)e;
         if (vec) {
-            kern::KernelFn pf = select_kernel(dp.h, dp.bcols, true, dp.ufk, true);
+            kern::KernelFn pf = select_kernel(dp.h, dp.bcols, true, dp.ufk, true, dp.colf);
             if (pf) cudaFuncSetAttribute((const void*)pf,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         }
@@ -146,7 +125,7 @@ int prepare_kernels(DevPlan& dp) {
 }
 
 int blocks_per_sm(const DevPlan& dp, bool vec, bool probe) {
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, probe);
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, probe, vec ? dp.colf : 0);
     if (!fn) return 1;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, 32 * dp.cta_warps,
@@ -170,7 +149,7 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
                 bool vec_ok, bool packed, float* const* extra, int n_extra, long long row_off,
                 bool multicast) {
     const bool vec = vec_ok && dp.variant == 1;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false);
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false, vec ? dp.colf : 0);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, vals, B, C, packed);
@@ -183,7 +162,7 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
 
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok) {
     if (!(vec_ok && dp.variant == 1)) return (int)cudaErrorInvalidConfiguration;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, true, dp.ufk, true);
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, true, dp.ufk, true, dp.colf);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
     kern::KParams p = make_params(dp, nullptr, B, sink);

@@ -334,6 +334,11 @@ Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm)
     const double g_est = (double)nnz;   // gcols at UFi = 1
     p.ufk = (bcols > 128 || g_est > 1.5e6) ? 4 : 8;
     if (bcols < 32) p.ufk = bcols == 4 ? 1 : bcols == 8 ? 2 : 4;   // UFk x (32 / (bCols/4)) <= 32
+    // bCols coarsening (columns per lane): on the large L1-wavefront-bound
+    // problems a 16-column register tile per lane (8 lanes per B row, 4 rows
+    // per warp instruction) halves the per-row broadcasts and issue
+    // (C4: 91.5 -> 83.6 us hot-L2, C5: 2.25 -> 2.14 ms; profiles/r1_notes.md)
+    p.colf = (bcols == 128 && g_est > 1.5e6) ? 16 : 0;
     const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
     const double target_items = 1536.0 * (double)n_sm / 148.0;

@@ -34,3 +34,28 @@ def test_c_client_device(client):
     r = subprocess.run([client, "device"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "device ok" in r.stdout
+
+
+def test_struct_layouts_match_binding(tmp_path):
+    """The ctypes mirrors of escs_params / escs_plan_stats / escs_plan_view
+    have the C compiler's size and field offsets (include/escs.h)."""
+    import ctypes
+    from paper_2506_15174_b200 import escs
+    structs = {"escs_params": escs._Params, "escs_plan_stats": escs._Stats,
+               "escs_plan_view": escs._View}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "escs.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = str(tmp_path / "layout")
+    subprocess.check_call(["gcc", "-std=c11", "-o", exe, str(src), "-I", os.path.join(ROOT, "include")])
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, f, v = line.split()
+        py = structs[cname]
+        got = ctypes.sizeof(py) if f == "size" else getattr(py, f).offset
+        assert got == int(v), (cname, f, got, v)

@@ -367,3 +367,31 @@ def test_fused_gather_symmetric_memory_world1(torch_cuda):
     torch.cuda.synchronize()
     ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B)
     assert np.array_equal(fg.C.cpu().numpy().astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("n,colf", [(32, 8), (64, 8), (64, 16), (128, 8), (128, 16), (256, 16),
+                                    (256, 8), (128, 4)])
+@pytest.mark.parametrize("T", [16, 0])
+def test_colf_lane_maps_exact(torch_cuda, n, colf, T):
+    """Every bCols coarsening factor (columns per lane of the vector map,
+    interleaved float4 chunks for colf > 4) against the oracle, bit-exact on
+    dyadic twins; T = 16 forces split panels (in-CTA combine) and, with
+    4-warp tiles, heavy panels combining through the workspace."""
+    A0 = synth.magnitude_pruned(777, 1500, 0.8, 51)
+    A, B = synth.dyadic_twin(A0, n, 52)
+    for warps in (4, 0):
+        C, pl = run_escs(torch_cuda, A, B, ufi=1, T=T, colf=colf, cta_warps=warps)
+        assert pl.info["colf"] == colf
+        if T and warps == 4:
+            assert pl.info["n_heavy"] > 0
+        check_exact(A, B, C)
+
+
+def test_autotuned_plan_reports_lane_map(torch_cuda):
+    from paper_2506_15174_b200 import escs
+    p = synth.transformer_suite(bcols=(128,), sparsities=(0.7,))[1]
+    A = p.A
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 128, autotune=1)
+    assert pl.info["autotuned"] == 1 and pl.info["colf"] in (4, 8, 16)
+    C, _ = run_escs(torch_cuda, A, p.B, autotune=1)
+    check_tol(A, p.B, C)

@@ -6,6 +6,7 @@ in csrc/plan.cpp (choose_params) is derived from these results.
     python tools/tune.py [--workload transformer] [--out gpurun_out/tune.json]
 """
 import argparse
+import itertools
 import json
 import os
 import sys
@@ -23,6 +24,7 @@ def main():
     ap.add_argument("--ufk", default="2,4,8")
     ap.add_argument("--T", default="0,8,16,32,64,128,256")
     ap.add_argument("--warps", default="0")
+    ap.add_argument("--colf", default="0", help="B columns per lane of the vector map (0 = default)")
     ap.add_argument("--filter", default="", help="comma-separated substrings of case names")
     ap.add_argument("--packed", action="store_true", help="time escs_spmm_packed (values pre-packed)")
     a = ap.parse_args()
@@ -48,32 +50,30 @@ def main():
         t_auto = bench.graph_time(torch, lambda: escs.escs_spmm(auto, dv, dB, dC, stream), stream,
                                   min_ms=1.0, reps=5)
         rec = {"case": p.name, "auto_us": 1e3 * t_auto,
-               "auto": {k: auto.info[k] for k in ("h", "T", "cta_warps", "ufk", "n_tiles")},
+               "auto": {k: auto.info[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles")},
                "grid": []}
         best = (t_auto, rec["auto"])
-        for ufi in map(int, a.ufi.split(",")):
-            for ufk in map(int, a.ufk.split(",")):
-                for T in map(int, a.T.split(",")):
-                    for w in map(int, a.warps.split(",")):
-                        try:
-                            pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n,
-                                                   ufi=ufi, ufk=ufk, T=T, cta_warps=w)
-                        except escs.EscsError:
-                            continue
-                        if a.packed:
-                            pv = torch.empty_like(dv)
-                            escs.escs_pack(pl, dv, pv, stream)
-                            fn = lambda: escs.escs_spmm_packed(pl, pv, dB, dC, stream)
-                        else:
-                            fn = lambda: escs.escs_spmm(pl, dv, dB, dC, stream)
-                        t = bench.graph_time(torch, fn, stream, min_ms=1.0, reps=5)
-                        inf = pl.info
-                        cfg = {"h": ufi, "ufk": ufk, "T": inf["T"], "cta_warps": inf["cta_warps"],
-                               "n_tiles": inf["n_tiles"], "n_heavy": inf["n_heavy"]}
-                        rec["grid"].append([1e3 * t, cfg])
-                        if t < best[0]:
-                            best = (t, cfg)
-                        pl.close()
+        grid = itertools.product(*(map(int, v.split(",")) for v in (a.ufi, a.ufk, a.T, a.warps, a.colf)))
+        for ufi, ufk, T, w, cf in grid:
+            try:
+                pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n,
+                                       ufi=ufi, ufk=ufk, T=T, cta_warps=w, colf=cf)
+            except escs.EscsError:
+                continue
+            if a.packed:
+                pv = torch.empty_like(dv)
+                escs.escs_pack(pl, dv, pv, stream)
+                fn = lambda: escs.escs_spmm_packed(pl, pv, dB, dC, stream)
+            else:
+                fn = lambda: escs.escs_spmm(pl, dv, dB, dC, stream)
+            t = bench.graph_time(torch, fn, stream, min_ms=1.0, reps=5)
+            inf = pl.info
+            cfg = {"h": ufi, "ufk": inf["ufk"], "T": inf["T"], "cta_warps": inf["cta_warps"],
+                   "colf": inf["colf"], "n_tiles": inf["n_tiles"], "n_heavy": inf["n_heavy"]}
+            rec["grid"].append([1e3 * t, cfg])
+            if t < best[0]:
+                best = (t, cfg)
+            pl.close()
         rec["best_us"] = 1e3 * best[0]
         rec["best"] = best[1]
         out.append(rec)
