@@ -18,8 +18,9 @@ struct BlSparse {
 };
 
 // Gather ceiling (bench roofline): warps gather pseudo-random 512-byte rows
-// (bCols 128, fp32) of an L2-resident B with no index loads, no values and
-// no FMAs -- the most B-row bytes per second the SM memory pipeline delivers
+// (bCols 128, fp32; row = fmix32(i) mod k, so repeats are spread like C5's
+// uniform columns and L1 reuse stays at its random-access level) of an
+// L2-resident B with no index loads, no values and no FMAs -- the most B-row bytes per second the SM memory pipeline delivers
 // to registers for this access pattern.  L lanes per row, 16 B per lane per
 // load instruction (interleaved), U rows in flight per sub-warp.
 template <int L, int U>
@@ -34,7 +35,9 @@ __global__ void __launch_bounds__(256) gather_peak_kernel(const float4* __restri
         float4 b[U][F4];
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            const unsigned r = (unsigned)((w * rows_per_warp + i + u * S + sub) * 2654435761ull) % (unsigned)k;
+            unsigned x = (unsigned)(w * rows_per_warp + i + u * S + sub);
+            x ^= x >> 16; x *= 0x85ebca6bu; x ^= x >> 13; x *= 0xc2b2ae35u; x ^= x >> 16;   // fmix32
+            const unsigned r = x % (unsigned)k;
 #pragma unroll
             for (int v = 0; v < F4; v++) b[u][v] = __ldg(B + (size_t)r * 32 + v * L + lj);
         }
