@@ -76,6 +76,8 @@ def workload(name):
         return synth.resnet_suite(), "configs[2]: ResNet-50 im2col 256x2304/512x4608/2048x512 x 70-98% x bCols 32/64/128"
     if name == "suite":
         return synth.suite(), "configs[1]+[2]: Transformer + ResNet-50 suites x bCols 32/64/128"
+    if name == "resnet50":
+        return synth.resnet50_full_suite(), "configs[2] extended: all 21 ResNet-50 GEMM shapes x 70-98% x bCols 32/64/128 (P:829)"
     if name == "wide":
         return synth.suite(bcols=(256,)), "suites at bCols 256 (beyond the north_star range; tuning only)"
     if name in ("c1", "c4", "c5"):
@@ -204,9 +206,10 @@ def geomean(xs):
     return math.exp(sum(math.log(x) for x in xs) / len(xs)) if xs else None
 
 
-def graph_time(torch, fn, stream, min_ms=2.0, reps=11):
+def graph_time(torch, fn, stream, min_ms=2.0, reps=11, stats=None):
     """Per-call time of fn (enqueue-only) with a CUDA graph of R calls,
-    replayed `reps` times (hot L2, the paper's warm-cache protocol P:675)."""
+    replayed `reps` times (hot L2, the paper's warm-cache protocol P:675).
+    Returns the median; `stats` (a dict) also receives min and p90."""
     with torch.cuda.stream(stream):
         for _ in range(3):
             fn()
@@ -235,6 +238,9 @@ def graph_time(torch, fn, stream, min_ms=2.0, reps=11):
         e.synchronize()
         ts.append(s.elapsed_time(e) / R)
     del g
+    if stats is not None:
+        q = sorted(ts)
+        stats.update(min=q[0], p90=q[min(len(q) - 1, int(math.ceil(0.9 * len(q))) - 1)], R=R, reps=reps)
     return statistics.median(ts)
 
 
@@ -289,7 +295,9 @@ def compare_baselines(torch, problems, dev, stream):
     for p in problems:
         A, n = p.A, p.bcols
         d = dev[p.name]
-        t_escs = graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream)
+        st_escs = {}
+        t_escs = graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream,
+                            reps=20, stats=st_escs)
         rp = torch.from_numpy(A.rowptr).to(dev["_device"])
         ci = torch.from_numpy(A.colidx).to(dev["_device"])
         Cs = torch.empty_like(d["C"])
@@ -312,14 +320,15 @@ def compare_baselines(torch, problems, dev, stream):
         t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
         del Ad
         inf = d["plan"].info
-        rows.append({"case": p.name, "escs_us": 1e3 * t_escs,
+        rows.append({"case": p.name, "escs_us": 1e3 * t_escs, "escs_us_min": 1e3 * st_escs["min"],
+                     "escs_us_p90": 1e3 * st_escs["p90"],
                      "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")},
                      "cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
                      "cublas_us": 1e3 * t_cublas, "cublas_tf32_us": 1e3 * t_tf32,
                      "gflops_escs": p.flops / (t_escs * 1e-3) / 1e9})
     bl.bl_cublas_destroy(cub)
     out = {
-        "protocol": "hot L2, CUDA graph of R calls replayed 11x, median (paper P:675 warm cache)",
+        "protocol": "hot L2, CUDA graph of R calls (R = clamp(2 ms / t, 10, 1000)) replayed 20x for escs, 11x for the baselines; median (paper P:675 warm cache); escs min and p90 per case",
         "geomean_speedup_vs_cusparse": geomean([r["cusparse_us"] / r["escs_us"] for r in rows if r["cusparse_us"]]),
         "geomean_speedup_vs_cublas": geomean([r["cublas_us"] / r["escs_us"] for r in rows]),
         "geomean_speedup_vs_cublas_tf32": geomean([r["cublas_tf32_us"] / r["escs_us"] for r in rows]),

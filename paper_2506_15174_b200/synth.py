@@ -21,12 +21,18 @@ import numpy as np
 __all__ = [
     "CSR", "Problem", "magnitude_pruned", "power_law", "uniform_large", "dense_b",
     "dyadic_twin", "transformer_suite", "resnet_suite", "suite", "config", "SPARSITIES",
-    "TRANSFORMER_SHAPES", "RESNET_SHAPES", "BCOLS",
+    "TRANSFORMER_SHAPES", "RESNET_SHAPES", "RESNET50_ALL_SHAPES", "BCOLS", "resnet50_full_suite",
 ]
 
 SPARSITIES = (0.70, 0.80, 0.90, 0.95, 0.98)
 TRANSFORMER_SHAPES = ((512, 512), (2048, 512), (512, 2048))        # P:664 "most common sizes"
 RESNET_SHAPES = ((256, 2304), (512, 4608), (2048, 512))             # im2col M x (C*kh*kw)
+# all 21 distinct ResNet-50 conv/fc GEMM shapes (M = out channels, K = in*kh*kw;
+# the paper's "21 different sizes"; SURVEY §8(d) C3 extended suite)
+RESNET50_ALL_SHAPES = ((64, 147), (64, 64), (64, 576), (256, 64), (64, 256), (128, 256),
+                       (128, 1152), (512, 128), (512, 256), (128, 512), (256, 512),
+                       (256, 2304), (1024, 256), (1024, 512), (256, 1024), (512, 1024),
+                       (512, 4608), (2048, 512), (2048, 1024), (512, 2048), (1000, 2048))
 BCOLS = (32, 64, 128)
 
 
@@ -225,6 +231,11 @@ def transformer_suite(bcols=BCOLS, sparsities=SPARSITIES):
 def resnet_suite(bcols=BCOLS, sparsities=SPARSITIES):
     """configs[2]: ResNet-50 im2col {256x2304, 512x4608, 2048x512}."""
     return _suite(RESNET_SHAPES, 3, bcols, sparsities)
+
+
+def resnet50_full_suite(bcols=BCOLS, sparsities=SPARSITIES):
+    """Extended configs[2]: every ResNet-50 layer shape (21) x sparsities x bCols."""
+    return _suite(RESNET50_ALL_SHAPES, 100, bcols, sparsities)
 
 
 def suite(bcols=BCOLS, sparsities=SPARSITIES):

@@ -395,3 +395,13 @@ def test_autotuned_plan_reports_lane_map(torch_cuda):
     assert pl.info["autotuned"] == 1 and pl.info["colf"] in (4, 8, 16)
     C, _ = run_escs(torch_cuda, A, p.B, autotune=1)
     check_tol(A, p.B, C)
+
+
+@pytest.mark.parametrize("n", [32, 128])
+def test_resnet50_all_shapes_exact(torch_cuda, n):
+    """All 21 ResNet-50 GEMM shapes (odd K such as 147 and 1152, M = 64
+    or 1000) at 70% and 95%, default plans, dyadic twins: bit-exact."""
+    for p in synth.resnet50_full_suite(bcols=(n,), sparsities=(0.7, 0.95)):
+        A, B = synth.dyadic_twin(p.A, n, 7)
+        C, _ = run_escs(torch_cuda, A, B)
+        check_exact(A, B, C)

@@ -304,3 +304,15 @@ def test_storage_trend_matches_paper_fig9():
         esc = 4 * hdr["nnz"] + 4 * hdr["G"] + 8 * (hdr["NG"] + 1) + 8 * hdr["NG"]
         csr = 8 * A.nnz + 4 * (m + 1)
         assert (esc < csr) == esc_smaller, (s, esc, csr)
+
+
+def test_resnet50_shape_list():
+    """The extended C3 suite: 21 distinct ResNet-50 GEMM shapes."""
+    from paper_2506_15174_b200 import synth
+    shapes = synth.RESNET50_ALL_SHAPES
+    assert len(shapes) == 21 and len(set(shapes)) == 21
+    assert set(synth.RESNET_SHAPES) <= set(shapes)
+    suite = synth.resnet50_full_suite(bcols=(32,), sparsities=(0.9,))
+    for p, (m, k) in zip(suite, shapes):
+        assert (p.A.m, p.A.k) == (m, k)
+        assert p.A.nnz == synth.nnz_for(m, k, 0.9)

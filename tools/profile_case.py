@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--config", default=None, help="c1/c4/c5 instead of a suite shape")
     ap.add_argument("--probe", action="store_true")
+    ap.add_argument("--shard", default=None, help="W/R: profile rank R's row block of W (SURVEY §8(e))")
     ap.add_argument("--case", default=None, help="a problem name from bench.py's workloads")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table (default: autotuned, as bench.py)")
@@ -25,7 +26,7 @@ def main():
     from paper_2506_15174_b200 import escs, synth
     if a.case:
         import bench
-        for wl in ("transformer", "resnet"):
+        for wl in ("transformer", "resnet", "resnet50"):
             hit = [q for q in bench.workload(wl)[0] if q.name == a.case]
             if hit:
                 A, B = hit[0].A, hit[0].B
@@ -39,6 +40,10 @@ def main():
         m, k = (int(x) for x in a.shape.split("x"))
         A = synth.magnitude_pruned(m, k, a.s, 1234)
         B = synth.dense_b(k, a.n, 99)
+    if a.shard:
+        world, rank = (int(x) for x in a.shard.split("/"))
+        r0, r1 = synth.shard_bounds(A.m, world, rank)
+        A = synth.row_block(A, r0, r1)
     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
                            autotune=1 if a.autotune else 0)
     print(pl.info, flush=True)
