@@ -569,17 +569,30 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
         for (int r = 0; r < H; r++)
 #pragma unroll
             for (int f = 0; f < F; f++) acc[r][f] = 0.f;
+        // partials summed in tile order (deterministic); D tiles' loads in
+        // flight at once (the walk's registers are dead here)
+        constexpr int D = H * F <= 16 ? 4 : H * F <= 32 ? 2 : 1;
 #pragma unroll 1
-        for (int t = 0; t < hv.z; t++) {
-            const float* part = p.ws + (size_t)(hv.y + t) * H * n;
+        for (int t0 = 0; t0 < hv.z; t0 += D) {
+            float q[D][H][F];
 #pragma unroll
-            for (int r = 0; r < H; r++)
-                if ((r % S) == sub)
+            for (int d = 0; d < D; d++) {
+                const float* part = p.ws + (size_t)(hv.y + min(t0 + d, hv.z - 1)) * H * n;
+#pragma unroll
+                for (int r = 0; r < H; r++)
 #pragma unroll
                     for (int f = 0; f < F; f++) {
                         const int j = Map::col(lj, f);
-                        if (Map::kVec || j < n) acc[r][f] += __ldcg(part + r * n + j);
+                        q[d][r][f] = ((r % S) == sub && (Map::kVec || j < n)) ? __ldcg(part + r * n + j) : 0.f;
                     }
+            }
+#pragma unroll
+            for (int d = 0; d < D; d++)
+                if (t0 + d < hv.z)
+#pragma unroll
+                    for (int r = 0; r < H; r++)
+#pragma unroll
+                        for (int f = 0; f < F; f++) acc[r][f] += q[d][r][f];
         }
         store_rows<H, Map>(p, hv.x, acc, sub, lj);
         if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
