@@ -182,7 +182,12 @@ typedef struct {
                              §3.4).  0 = default (4; 8 at bCols 256); 8 or 16
                              at bCols 32..256 (UFi = 1 only).  Searched by the
                              autotuner when 0.                                  */
-    int32_t reserved[3];  /* must be zero                                        */
+    int32_t tile_order;   /* CTA tile formation: 0 = auto (by item length when the
+                             panel work is skewed, p99 >= 2x median), 1 = panel
+                             order, 2 = panels ordered by their longest item
+                             (similar work per tile, long tiles first).
+                             Searched by the autotuner when 0.               */
+    int32_t reserved[2];  /* must be zero                                        */
 } escs_params;
 
 /* escs_plan with explicit parameters; p may be NULL (= all auto). */
@@ -224,6 +229,7 @@ typedef struct {
     int32_t ctas_per_sm;    /* resident CTAs per SM of the launch (occupancy), 0 host-only */
     int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing */
     int32_t colf;           /* B columns per lane of the launch's lane map (0 scalar map) */
+    int32_t tile_order;     /* 1 panel order, 2 by item length (resolved)          */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);

@@ -66,6 +66,7 @@ void apply_env(escs::Params& p, bool& set_warps) {
             else if (k == "variant") p.variant = v;
             else if (k == "ufk") p.ufk = v;
             else if (k == "colf") p.colf = v;
+            else if (k == "order") p.tile_order = v;
         }
         i = j + 1;
     }
@@ -78,6 +79,24 @@ void apply_env(escs::Params& p, bool& set_warps) {
 // through the workspace (C4: 117 -> 92 us, profiles/r1_tune_c4.json).
 // (16-warp tiles packing several panels were measured too: faster only when
 // they remove a second wave, slower otherwise -- profiles/r1_tune_big.json.)
+// Tile order: by item length when panel work is skewed (power-law rows, C4:
+// 96 -> 82 us), else panel order (uniform layers: within noise, slightly
+// better in panel order).  p99 vs median of the panels' stream lengths.
+int auto_tile_order(const escs::PlanHost& ph) {
+    const int64_t nP = ph.header[7];
+    const int64_t NI = ph.item_panel.size();
+    if (nP < 2) return 1;
+    std::vector<int32_t> len(nP, 0);
+    for (int64_t i = 0; i < NI; i++)
+        len[ph.item_panel[i]] += ph.item_gcol_ptr[i + 1] - ph.item_gcol_ptr[i];
+    const int64_t k99 = std::min<int64_t>(nP - 1, (nP * 99) / 100);
+    std::nth_element(len.begin(), len.begin() + k99, len.end());
+    const int32_t p99 = len[k99];
+    std::nth_element(len.begin(), len.begin() + nP / 2, len.begin() + k99);
+    const int32_t med = std::max(1, len[nP / 2]);
+    return p99 >= 2 * med ? 2 : 1;
+}
+
 int auto_cta_warps(const escs::PlanHost& ph) {
     const int64_t nP = ph.header[7];
     const int64_t NI = ph.item_panel.size();
@@ -201,7 +220,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         return nullptr;
     }
     if (ep) {
-        for (int i = 0; i < 3; i++)
+        for (int i = 0; i < 2; i++)
             if (ep->reserved[i] != 0) {
                 fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
                 return nullptr;
@@ -231,11 +250,14 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         if (ep->variant) p.variant = ep->variant;
         if (ep->ufk) p.ufk = ep->ufk;
         if (ep->colf) p.colf = ep->colf;
+        if (ep->tile_order) p.tile_order = ep->tile_order;
         if (ep->nthreads) p.nthreads = ep->nthreads;
     }
     if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > 16)) ||
-        p.variant < 1 || p.variant > 2) {
-        fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16, variant 1..2)");
+        p.variant < 1 || p.variant > 2 || p.tile_order < 0 || p.tile_order > 2 ||
+        !(p.colf == 0 || p.colf == 4 || p.colf == 8 || p.colf == 16)) {
+        fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16, "
+                           "variant 1..2, colf 0/4/8/16, tile_order 0..2)");
         return nullptr;
     }
     if (p.variant == 1 && !(bCols == 4 || bCols == 8 || bCols == 16 || bCols == 32 || bCols == 64 ||
@@ -266,7 +288,11 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     try {
         escs::build_plan(m, k, nnz, rowptr, colidx, bCols, p, P->host);
         if (!set_warps) p.cta_warps = auto_cta_warps(P->host);
-        escs::build_tiles(P->host, p.cta_warps);
+        const char* to = std::getenv("ESCS_TILE_ORDER");   // "panel" | "length" override
+        if (to && std::string(to) == "panel") p.tile_order = 1;
+        else if (to && std::string(to) == "length") p.tile_order = 2;
+        if (p.tile_order < 1 || p.tile_order > 2) p.tile_order = auto_tile_order(P->host);
+        escs::build_tiles(P->host, p.cta_warps, p.tile_order == 2);
     } catch (const std::bad_alloc&) {
         delete P;
         fail(ESCS_ERR_OOM, "host allocation while planning");
@@ -440,6 +466,17 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             }
         }
     }
+    // stage 5: tile order (panel order vs panels by longest item)
+    if (!(ep && ep->tile_order)) {
+        escs_params c = q;
+        c.ufi = best->params.h;
+        c.T = best->params.T;
+        c.cta_warps = best->params.cta_warps;
+        c.ufk = best->params.ufk;
+        c.colf = best->dev.variant == 1 ? best->params.colf : 0;
+        c.tile_order = best->params.tile_order == 2 ? 1 : 2;
+        consider(c);
+    }
     best->autotuned = true;
     clear_error();
     return best;
@@ -600,6 +637,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false);
     o->autotuned = plan->autotuned ? 1 : 0;
     o->colf = plan->dev.variant == 1 ? plan->params.colf : 0;
+    o->tile_order = plan->params.tile_order;
     return ESCS_OK;
 }
 

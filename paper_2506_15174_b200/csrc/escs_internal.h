@@ -15,6 +15,7 @@ struct Params {
     int variant = 1;    // 1 = vector (float4) lane map, 2 = scalar lane map
     int ufk = 4;        // B-row loads in flight per sub-warp step (UFk)
     int colf = 0;       // B columns per lane of the vector map (bCols coarsening), 0 = default
+    int tile_order = 0; // 0 auto, 1 panel order, 2 by longest item
     int nthreads = 0;   // planner threads
 };
 
@@ -47,7 +48,7 @@ void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm);
 
 // Pick cta_warps from the item distribution and build the tile schedule.
-void build_tiles(PlanHost& ph, int cta_warps);
+void build_tiles(PlanHost& ph, int cta_warps, bool by_length = true);
 
 // Device-side view used by the kernels.
 struct DevPlan {

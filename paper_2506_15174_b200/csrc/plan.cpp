@@ -240,7 +240,7 @@ void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr, const 
 // shared memory by one CTA.  A panel with more than W items ("heavy", the
 // power-law case C4) gets ceil(n/W) exclusive tiles that are combined through
 // a global workspace in tile order (deterministic fixup).
-void build_tiles(PlanHost& ph, int W) {
+void build_tiles(PlanHost& ph, int W, bool by_length) {
     const int64_t NI = ph.item_panel.size();
     const int64_t nP = ph.header[7];
     ph.slot_item.clear();
@@ -250,8 +250,6 @@ void build_tiles(PlanHost& ph, int W) {
     ph.n_heavy = ph.n_heavy_tiles = ph.n_split_items = 0;
     ph.any_sync = false;
     std::vector<int32_t> lc(NI, 0);      // lead | cnt << 8 per item
-    std::vector<int64_t> cur;            // items of the open tile
-    bool cur_sync = false;
     auto emit = [&](const std::vector<int64_t>& its, bool sync, int hid, int q) {
         for (int k = 0; k < W; k++) {
             if (k < (int)its.size()) {
@@ -267,44 +265,66 @@ void build_tiles(PlanHost& ph, int W) {
         ph.tile_heavy.push_back(q);
         ph.any_sync |= sync;
     };
-    auto close = [&]() {
-        if (!cur.empty()) emit(cur, cur_sync, -1, 0);
-        cur.clear();
-        cur_sync = false;
-    };
-    int64_t i = 0;
+    // panels' item ranges (items are ordered by panel)
+    std::vector<int64_t> first(nP + 1, NI);
+    for (int64_t i = NI - 1; i >= 0; i--) first[ph.item_panel[i]] = i;
+    first[nP] = NI;
+    for (int64_t P = nP - 1; P >= 0; P--)
+        if (first[P] > first[P + 1]) first[P] = first[P + 1];
+    // heavy panels (more items than warps): their own tiles, combined through
+    // the workspace; emitted first -- they are the longest chains
+    std::vector<int64_t> light;
+    light.reserve(nP);
     for (int64_t P = 0; P < nP; P++) {
-        const int64_t a = i;
-        while (i < NI && ph.item_panel[i] == P) i++;
-        const int64_t n = i - a;
+        const int64_t a = first[P], n = first[P + 1] - a;
         if (n > 1) ph.n_split_items += (int32_t)n;
-        if (n > W) {
-            close();
-            const int64_t nt = (n + W - 1) / W;
-            const int hid = ph.n_heavy++;
-            ph.heavy_info.insert(ph.heavy_info.end(),
-                                 {(int32_t)P, ph.n_heavy_tiles, (int32_t)nt, 0});
-            for (int64_t q = 0; q < nt; q++) {
-                const int64_t b0 = a + (q * n) / nt, b1 = a + ((q + 1) * n) / nt;
-                std::vector<int64_t> its;
-                for (int64_t j = b0; j < b1; j++) {
-                    lc[j] = 0 | ((int32_t)(b1 - b0) << 8);
-                    its.push_back(j);
-                }
-                emit(its, true, hid, (int)q);
-            }
-            ph.n_heavy_tiles += (int32_t)nt;
+        if (n <= W) {
+            light.push_back(P);
             continue;
         }
-        if ((int64_t)cur.size() + n > W) close();
+        const int64_t nt = (n + W - 1) / W;
+        const int hid = ph.n_heavy++;
+        ph.heavy_info.insert(ph.heavy_info.end(), {(int32_t)P, ph.n_heavy_tiles, (int32_t)nt, 0});
+        for (int64_t q = 0; q < nt; q++) {
+            const int64_t b0 = a + (q * n) / nt, b1 = a + ((q + 1) * n) / nt;
+            std::vector<int64_t> its;
+            for (int64_t j = b0; j < b1; j++) {
+                lc[j] = 0 | ((int32_t)(b1 - b0) << 8);
+                its.push_back(j);
+            }
+            emit(its, true, hid, (int)q);
+        }
+        ph.n_heavy_tiles += (int32_t)nt;
+    }
+    // light panels: whole panels packed W item slots per tile.  With
+    // by_length, panels are ordered by their longest item (descending, ties by
+    // panel) so that a tile's warps carry similar work -- a CTA holds its SM
+    // slot until its longest warp finishes -- and long tiles start first.
+    if (by_length) {
+        std::vector<int32_t> len(nP, 0);
+        for (int64_t P : light)
+            for (int64_t j = first[P]; j < first[P + 1]; j++)
+                len[P] = std::max(len[P], ph.item_gcol_ptr[j + 1] - ph.item_gcol_ptr[j]);
+        std::stable_sort(light.begin(), light.end(),
+                         [&](int64_t x, int64_t y) { return len[x] > len[y]; });
+    }
+    std::vector<int64_t> cur;
+    bool cur_sync = false;
+    for (int64_t P : light) {
+        const int64_t a = first[P], n = first[P + 1] - a;
+        if ((int64_t)cur.size() + n > W) {
+            emit(cur, cur_sync, -1, 0);
+            cur.clear();
+            cur_sync = false;
+        }
         const int32_t lead = (int32_t)cur.size();
-        for (int64_t j = a; j < i; j++) {
+        for (int64_t j = a; j < a + n; j++) {
             lc[j] = lead | ((int32_t)n << 8);
             cur.push_back(j);
         }
         if (n > 1) cur_sync = true;
     }
-    close();
+    if (!cur.empty()) emit(cur, cur_sync, -1, 0);
     ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 

@@ -35,7 +35,8 @@ class _Params(ctypes.Structure):
     _fields_ = [("ufi", ctypes.c_int32), ("T", ctypes.c_int32), ("host_only", ctypes.c_int32),
                 ("cta_warps", ctypes.c_int32), ("variant", ctypes.c_int32), ("ufk", ctypes.c_int32),
                 ("nthreads", ctypes.c_int32), ("autotune", ctypes.c_int32),
-                ("colf", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("colf", ctypes.c_int32), ("tile_order", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class _View(ctypes.Structure):
@@ -49,7 +50,8 @@ class _Stats(ctypes.Structure):
                [(n, ctypes.c_int64) for n in ("nP", "NG", "G", "n_items", "nnz", "device_bytes",
                                               "workspace_bytes")] + \
                [("plan_seconds", ctypes.c_double), ("ctas_per_sm", ctypes.c_int32),
-                ("autotuned", ctypes.c_int32), ("colf", ctypes.c_int32)]
+                ("autotuned", ctypes.c_int32), ("colf", ctypes.c_int32),
+                ("tile_order", ctypes.c_int32)]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -144,10 +146,10 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
-                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0) -> Plan:
+                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0) -> Plan:
     rowptr, colidx = _csr_args(rowptr, colidx)
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
-                int(nthreads), int(autotune), int(colf), (ctypes.c_int32 * 3)())
+                int(nthreads), int(autotune), int(colf), int(tile_order), (ctypes.c_int32 * 2)())
     h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
                           int(bCols), ctypes.byref(p))
     if not h:

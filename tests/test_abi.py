@@ -104,3 +104,19 @@ def test_tiles_cover_items():
     info = pl.info
     assert info["n_heavy"] > 0
     assert info["n_tiles"] >= -(-info["n_items"] // 4)
+
+
+def test_params_out_of_range_rejected():
+    """escs_plan_ex rejects out-of-range tuning parameters with ESCS_ERR_ARG
+    (host-only plans: no GPU needed)."""
+    import pytest
+    from paper_2506_15174_b200 import escs, synth
+    A = synth.random_csr(20, 30, 100, 1)
+    for bad in ({"colf": 5}, {"tile_order": 3}, {"cta_warps": 17}, {"variant": 3}):
+        with pytest.raises(escs.EscsError) as e:
+            escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **bad)
+        assert e.value.code == escs.ESCS_ERR_ARG
+    for ok in ({"colf": 8}, {"tile_order": 2}, {"tile_order": 1}):
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **ok)
+        assert pl.info["tile_order"] in (1, 2)
+        pl.close()

@@ -192,9 +192,13 @@ def test_unaligned_pointers_take_scalar_path(torch_cuda):
     check_exact(A, B, bufC[1:].cpu().numpy().reshape(A.m, 64))
 
 
-def test_c4_full_size(torch_cuda):
+@pytest.mark.parametrize("autotune", [0, 1])
+def test_c4_full_size(torch_cuda, autotune):
+    """C4 at full size, default plan and the autotuned plan bench.py times
+    (heavy panels, 16-column lane tiles): sampled rows incl. every dense row."""
     p = synth.config("c4")
-    C, pl = run_escs(torch_cuda, p.A, p.B)
+    prm = {"autotune": 1} if autotune else {}
+    C, pl = run_escs(torch_cuda, p.A, p.B, **prm)
     info = pl.info
     rng = np.random.default_rng(0)
     lens = np.diff(p.A.rowptr)
@@ -202,10 +206,10 @@ def test_c4_full_size(torch_cuda):
                                      np.argsort(lens)[-24:]]))    # include every dense row
     check_tol(p.A, p.B, C, rows=rows)
     A, B = synth.dyadic_twin(p.A, 128, 17)
-    C, _ = run_escs(torch_cuda, A, B)
+    C, _ = run_escs(torch_cuda, A, B, **prm)
     ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B, rows=rows)
     assert np.array_equal(C[rows].astype(np.float64), ref)
-    assert info["n_tiles"] > 0
+    assert info["n_tiles"] > 0 and info["n_heavy"] > 0
 
 
 def test_rowblock_shards_stitch(torch_cuda):
@@ -405,3 +409,15 @@ def test_resnet50_all_shapes_exact(torch_cuda, n):
         A, B = synth.dyadic_twin(p.A, n, 7)
         C, _ = run_escs(torch_cuda, A, B)
         check_exact(A, B, C)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("warps", [2, 4, 16])
+def test_tile_order_exact(torch_cuda, order, warps):
+    """Both CTA tile formations (panel order; panels by longest item) on
+    power-law rows with split and heavy panels: bit-exact (dyadic twin)."""
+    A0 = synth.power_law(3000, 2000, 0.97, 61)
+    A, B = synth.dyadic_twin(A0, 128, 62)
+    C, pl = run_escs(torch_cuda, A, B, ufi=1, T=24, cta_warps=warps, tile_order=order)
+    assert pl.info["tile_order"] == order
+    check_exact(A, B, C)
