@@ -409,7 +409,7 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         const double sp = nP > 0 ? (double)best->host.header[9] / nP : 0.0;
         std::vector<int> cand;
         const int T0 = best->params.T;
-        for (double f : {0.35, 0.5, 0.7, 1.4, 2.0, 3.0}) cand.push_back(std::max(8, (int)(T0 * f)));
+        for (double f : {0.35, 0.5, 0.7, 1.4, 2.0, 3.0, 5.0}) cand.push_back(std::max(8, (int)(T0 * f)));
         for (int per : {1, 2, 3, 4, 6, 8})
             if (sp >= 1.0) cand.push_back(std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / per)));
         std::sort(cand.begin(), cand.end());
