@@ -672,6 +672,18 @@ def run_escs(args):
             v, reps, secs, thr = oracle_time(problems, budget_s=args.cpu_budget)
             result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
                                       "sample": f"whole workload x{reps} ({secs:.1f} s), fp64 C oracle"}
+            # one-time planning costs (the paper excludes its dataTransformer from
+            # SpMM time): escs_plan (h-way merge, threaded, incl. autotuning)
+            # vs the oracle's dense-scan partitioner (O(m*k) per problem)
+            if sum(p.A.m * p.A.k for p in problems) <= 2e9:
+                import oracle
+                t0 = time.perf_counter()
+                for p, d in shard_problems:
+                    inf = d["plan"].info
+                    oracle.partition(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, inf["h"], inf["T"], p.bcols)
+                result["planning"] = {"escs_plan_s": plan_s,
+                                      "oracle_partition_s": time.perf_counter() - t0,
+                                      "what": "one-time host planning for the whole workload (not in value)"}
         if world == 1 and not args.no_compare:
             summ, rows = compare_baselines(torch, problems, dev, stream)
             result["baselines"] = summ
