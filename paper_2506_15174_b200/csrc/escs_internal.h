@@ -78,6 +78,7 @@ int prepare_kernels(DevPlan& dp);
 // Does a kernel instance exist for this configuration?
 bool kernel_supported(int h, int bcols, int variant, int ufk, int colf);
 int default_colf(int bcols);
+int launch_spin(void* stream, long long cycles);   // tuner: busy-wait on the stream
 size_t smem_bytes(const DevPlan& dp);
 // Resident CTAs per SM for this plan's launch configuration.
 int blocks_per_sm(const DevPlan& dp, bool vec, bool probe);

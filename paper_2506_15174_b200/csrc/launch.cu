@@ -19,6 +19,15 @@ __global__ void __launch_bounds__(256) esc_pack_kernel(const int* __restrict__ s
         out[s] = vals[ld_stream(slot + s)];
 }
 
+// Busy-wait kernel for the plan-time tuner: occupies the stream while the
+// host enqueues a batch of launches, so the timed batch measures GPU time,
+// not host launch rate (microsecond-scale layers launch slower than they run).
+__global__ void spin_kernel(long long cycles) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles) {
+    }
+}
+
 }  // namespace kern
 
 namespace {
@@ -76,6 +85,11 @@ int launch(kern::KernelFn fn, const DevPlan& dp, const kern::KParams& p, size_t 
 }  // namespace
 
 int default_colf(int bcols) { return kern::default_colf(bcols); }
+
+int launch_spin(void* stream, long long cycles) {
+    kern::spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(cycles);
+    return (int)cudaGetLastError();
+}
 
 bool kernel_supported(int h, int bcols, int variant, int ufk, int colf) {
     if (h < 1 || h > 4 || bcols < 1 || bcols > 256) return false;
