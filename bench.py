@@ -148,7 +148,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- reference arm
 
-def oracle_time(problems, budget_s=8.0, max_reps=50):
+def oracle_time(problems, budget_s=10.0, max_reps=1000):
     """Time the fp64 CPU oracle over the whole workload (repeated until about
     budget_s of CPU work).  Returns (GFLOP/s, reps, seconds, threads)."""
     import oracle
@@ -752,7 +752,7 @@ def main(argv=None):
     ap.add_argument("--workload", default="suite")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=8.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--cases-out", default=None)
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table only (default: plan-time autotuning)")
