@@ -220,44 +220,6 @@ struct Stage {
     float w[2][32][HP];
 };
 
-// Load chunk `c` of the item into registers (packed word + row values of
-// this lane's column).  Slots of a panel's stream are contiguous in stream
-// order, popcount(mask) per column, pattern rows ascending (Reading R1), so
-// the lane's first slot is the chunk base plus an exclusive warp scan of the
-// popcounts.  Returns the slot base of the next chunk.
-template <int H, bool PROBE>
-__device__ __forceinline__ int fetch_chunk(const KParams& p, const int* gp, int n, int c0,
-                                           int sbase, int lane, int& pk, float (&w)[H]) {
-    pk = (c0 + lane < n) ? ld_stream(gp + c0 + lane) : 0;
-    const unsigned mask = (unsigned)pk >> kColBits;
-    if constexpr (PROBE) {
-#pragma unroll
-        for (int r = 0; r < H; r++) w[r] = 0.f;
-        return sbase;
-    } else {
-        const unsigned lt = (1u << lane) - 1u;
-        int excl = 0, total = 0;
-#pragma unroll
-        for (int bit = 0; bit < 3; bit++) {
-            const unsigned bal = __ballot_sync(kFull, (__popc(mask) >> bit) & 1);
-            excl += __popc(bal & lt) << bit;
-            total += __popc(bal) << bit;
-        }
-        // packed values (escs_pack, the paper's ANNZ) are read contiguously;
-        // CSR-ordered values through the slot map
-        const int* sp = p.slot + sbase + excl;
-        const float* pv = p.vals + sbase + excl;
-#pragma unroll
-        for (int r = 0; r < H; r++) {
-            const int rank = __popc(mask & ((1u << r) - 1u));
-            float x = 0.f;
-            if ((mask >> r) & 1u) x = ld_stream_f(p.packed ? pv + rank : p.vals + ld_stream(sp + rank));
-            w[r] = x;
-        }
-        return sbase + total;
-    }
-}
-
 template <int H>
 __device__ __forceinline__ void put_chunk(Stage<H>& st, int buf, int lane, int pk,
                                           const float (&w)[H]) {
@@ -367,6 +329,39 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
 // so structural zeros are never multiplied and the code stays one compact
 // body for all 2^UFi - 1 patterns.  The next chunk's columns and values are
 // fetched while the current chunk computes.
+// Operand pipeline of the UFi > 1 walk, three chunks deep: while chunk c
+// computes, the values of chunk c+1 (addresses known), the slot-map entries
+// of chunk c+2 (packed words known) and the packed words of chunk c+3 are in
+// flight, so no dependent global round trip sits between two chunks' FMAs.
+// slot_addr: this lane's value positions for a chunk (exclusive warp scan of
+// the popcounts, Reading R1 order) -- the slot-map loads for CSR-ordered
+// values, or the positions themselves when the values are pre-packed.
+template <int H>
+__device__ __forceinline__ int slot_addr(const KParams& p, int pk, int sbase, int lane,
+                                         int (&sl)[H]) {
+    const unsigned mask = (unsigned)pk >> kColBits;
+    const unsigned lt = (1u << lane) - 1u;
+    int excl = 0, total = 0;
+#pragma unroll
+    for (int bit = 0; bit < 3; bit++) {
+        const unsigned bal = __ballot_sync(kFull, (__popc(mask) >> bit) & 1);
+        excl += __popc(bal & lt) << bit;
+        total += __popc(bal) << bit;
+    }
+#pragma unroll
+    for (int r = 0; r < H; r++) {
+        const int pos = sbase + excl + __popc(mask & ((1u << r) - 1u));
+        sl[r] = ((mask >> r) & 1u) ? (p.packed ? pos : ld_stream(p.slot + pos)) : -1;
+    }
+    return sbase + total;
+}
+
+template <int H>
+__device__ __forceinline__ void load_vals(const KParams& p, const int (&sl)[H], float (&w)[H]) {
+#pragma unroll
+    for (int r = 0; r < H; r++) w[r] = sl[r] >= 0 ? ld_stream_f(p.vals + sl[r]) : 0.f;
+}
+
 template <int H, class Map, int U, bool PROBE>
 __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, int end, int sbase,
                                      float (&acc)[H][Map::F], int lane) {
@@ -375,17 +370,36 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
     const int sub = lane / Map::L, lj = lane % Map::L;
     const int n = end - beg;
     const int* gp = p.gpk + beg;
-    int pk;
-    float w[H];
+    // plan words of chunks 0..2 (immutable plan: before the PDL wait)
+    int pkA = lane < n ? ld_stream(gp + lane) : 0;
+    int pkB = 32 + lane < n ? ld_stream(gp + 32 + lane) : 0;
+    int pkC = 64 + lane < n ? ld_stream(gp + 64 + lane) : 0;
     grid_dep_wait();
-    sbase = fetch_chunk<H, PROBE>(p, gp, n, 0, sbase, lane, pk, w);
-    put_chunk<H>(st, 0, lane, pk, w);
+    float w[H];
+    int slA[H], slB[H];
+    if constexpr (PROBE) {
+#pragma unroll
+        for (int r = 0; r < H; r++) { w[r] = 0.f; slB[r] = -1; }
+    } else {
+        sbase = slot_addr<H>(p, pkA, sbase, lane, slA);
+        sbase = slot_addr<H>(p, pkB, sbase, lane, slB);
+        load_vals<H>(p, slA, w);
+    }
+    put_chunk<H>(st, 0, lane, pkA, w);
     __syncwarp();
     int buf = 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < n; c0 += 32) {
         const bool more = c0 + 32 < n;
-        if (more) sbase = fetch_chunk<H, PROBE>(p, gp, n, c0 + 32, sbase, lane, pk, w);
+        if (more) {
+            if constexpr (!PROBE) {
+                load_vals<H>(p, slB, w);                        // chunk c+1
+                if (c0 + 64 < n) sbase = slot_addr<H>(p, pkC, sbase, lane, slB);   // chunk c+2
+            }
+        }
+        const int pkN = pkB;
+        pkB = pkC;
+        pkC = c0 + 96 + lane < n ? ld_stream(gp + c0 + 96 + lane) : 0;   // chunk c+3
         const int cn = min(32, n - c0);
         // columns past the item end have pk = 0: row 0 is loaded, pattern 0
         // predicates every FMA off
@@ -416,7 +430,7 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
             }
         }
         if (more) {
-            put_chunk<H>(st, buf ^ 1, lane, pk, w);
+            put_chunk<H>(st, buf ^ 1, lane, pkN, w);
             __syncwarp();
             buf ^= 1;
         }
@@ -571,7 +585,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
             for (int f = 0; f < F; f++) acc[r][f] = 0.f;
         // partials summed in tile order (deterministic); D tiles' loads in
         // flight at once (the walk's registers are dead here)
-        constexpr int D = H * F <= 16 ? 4 : H * F <= 32 ? 2 : 1;
+        constexpr int D = H * F <= 8 ? 4 : H * F <= 16 ? 2 : 1;
 #pragma unroll 1
         for (int t0 = 0; t0 < hv.z; t0 += D) {
             float q[D][H][F];
