@@ -13,7 +13,9 @@ resident in HBM.  Default workload: the layer suite BASELINE.json's metric
 at {70,80,90,95,98}% x bCols {32,64,128} = 90 SpMMs per step.  With N>1 ranks (torchrun), every
 problem is row-block sharded (rank r owns rows [r*m/N, (r+1)*m/N), B
 replicated, no collective on the hot path): total work is
-fixed, so scaling is "strong".
+fixed, so scaling is "strong".  The independent problems of a suite run on
+--streams S streams (default 4, LPT by flops; forked from and joined into the
+timed stream); the same steps on one stream are reported as "serial".
 
 Timing: W untimed warm-up steps, then K timed steps.  Before each step the L2
 is flushed by writing a 256 MiB buffer (> 126 MB L2), and a device-side sleep
@@ -404,13 +406,40 @@ def run_escs(args):
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)
 
-    def step(per_launch=None):
+    # --streams S > 1: the independent problems of a suite run on S streams
+    # (LPT by flops), forked from and joined back into the timed stream, so
+    # small latency-bound layers overlap on the SMs (the suite analogue of the
+    # problem partition across ranks).  Each stream chains its launches with PDL.
+    nstreams = max(1, min(args.streams, len(shard_problems)))
+    lanes = [stream] + [torch.cuda.Stream(device) for _ in range(nstreams - 1)]
+    groups = shard.partition_problems([d["flops"] for _, d in shard_problems], nstreams)
+    owner = {i: g for g, idx in enumerate(groups) for i in idx}
+
+    def step(per_launch=None, serial=False):
+        if serial:      # every launch on the timed stream (the 1-stream figure)
+            for i, (p, d) in enumerate(shard_problems):
+                if per_launch is not None:
+                    per_launch[i][0].record(stream)
+                escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
+                if per_launch is not None:
+                    per_launch[i][1].record(stream)
+            return
+        if nstreams > 1:
+            fork = torch.cuda.Event()
+            fork.record(stream)
+            for s_ in lanes[1:]:
+                s_.wait_event(fork)
         for i, (p, d) in enumerate(shard_problems):
+            st = lanes[owner[i]]
             if per_launch is not None:
-                per_launch[i][0].record(stream)
-            escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
+                per_launch[i][0].record(st)
+            escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], st)
             if per_launch is not None:
-                per_launch[i][1].record(stream)
+                per_launch[i][1].record(st)
+        for s_ in lanes[1:]:
+            j = torch.cuda.Event()
+            j.record(s_)
+            stream.wait_event(j)
 
     def barrier():
         if world > 1:
@@ -439,12 +468,25 @@ def run_escs(args):
             ends[s].record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
-        # ---- timed again with per-launch events (kernel durations for the roofline)
+        # ---- the same steps with every launch on one stream (reported beside value)
+        serial_ms = None
+        if nstreams > 1:
+            s0, s1 = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+            for s in range(args.steps):
+                flush.zero_()
+                torch.cuda._sleep(sleep_cycles)
+                s0[s].record(stream)
+                step(serial=True)
+                s1[s].record(stream)
+            barrier()
+            serial_ms = sum(a.elapsed_time(b) for a, b in zip(s0, s1))
+        # ---- timed again with per-launch events (kernel durations for the roofline;
+        # one stream, so each duration is the kernel alone)
         pl_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
         for s in range(args.steps):
             flush.zero_()
             torch.cuda._sleep(sleep_cycles)
-            step(pl_ev[s])
+            step(pl_ev[s], serial=True)   # kernels alone, like the probe below
         barrier()
     # ---- gather probe: same walk and B-row loads, no values/FMAs (t_probe)
     probe_ms = None
@@ -643,7 +685,8 @@ def run_escs(args):
     # ---- reduce over ranks: flops SUM, times MAX
     my_flops = sum(d["flops"] for _, d in shard_problems)
     my_bytes = sum(d["bytes"] for _, d in shard_problems)
-    total_ms, e2e_ms, kern_ms_sum = shard.max_over_ranks([total_ms, e2e_ms, kern_ms_sum], device)
+    total_ms, e2e_ms, kern_ms_sum, serial_ms = shard.max_over_ranks(
+        [total_ms, e2e_ms, kern_ms_sum, serial_ms or 0.0], device)
     flops_all, bytes_all = shard.sum_over_ranks([my_flops, my_bytes], device)
 
     result = None
@@ -672,6 +715,7 @@ def run_escs(args):
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "problems": len(problems), "sharding": sharding,
+                       "streams": nstreams,
                        "l2": "flushed before every step (256 MiB write); each problem touched once per step",
                        "plans": ("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates)"
                                  if args.autotune else "parameter table (escs_plan defaults)"),
@@ -679,8 +723,8 @@ def run_escs(args):
             "roofline": {"bound": "hbm", "achieved": step_bytes_per_s, "peak": hbm, "unit": "GB/s",
                          "frac": step_bytes_per_s / hbm, "traffic": traffic,
                          "achieved_how": ("algorithmic bytes of the step / timed step (CUDA events on the "
-                                          "launching stream; the timed region holds only escs_spmm launches, "
-                                          "back to back with PDL)"),
+                                          "launching streams; the timed region holds only escs_spmm launches, "
+                                          "back to back with PDL on each of config.streams streams)"),
                          "achieved_per_launch_bracketed": achieved,
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": my_bytes / nprob,
@@ -688,6 +732,7 @@ def run_escs(args):
                          "algorithmic_bytes": "8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols per launch (CSR A, B, C once; SURVEY 8(d))",
                          "kernel": "escs_spmm (esc_spmm_kernel), all launches of the step",
                          "kernel_ms_per_step": float(kern_ms.sum() / K),
+                         "kernel_ms_how": "sum of per-launch CUDA-event durations, launches on one stream (each kernel alone)",
                          "gather_GBps": gather,
                          "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)",
                          "gather_roofline": {
@@ -709,6 +754,10 @@ def run_escs(args):
                                    "the copies alone")},
             "plan_seconds": plan_s,
         }
+        if nstreams > 1:
+            result["serial"] = {"value": flops_all * K / (serial_ms * 1e-3) / 1e9, "unit": UNIT,
+                                "ms_per_step": serial_ms / K,
+                                "what": "same steps, every escs_spmm on one stream (PDL chain)"}
         if allgather_ms is not None:
             result["allgather_ms_per_step"] = allgather_ms
         if fused is not None:
@@ -753,6 +802,8 @@ def main(argv=None):
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--streams", type=int, default=4,
+                    help="suite: run the independent problems on this many streams (LPT by flops)")
     ap.add_argument("--cases-out", default=None)
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table only (default: plan-time autotuning)")
