@@ -401,7 +401,7 @@ def run_escs(args):
              "gather_bytes": 4 * p.bcols * info["G"]}
         dev[p.name] = d
         shard_problems.append((p, d))
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=device)
+    flush = torch.empty(L2_FLUSH_BYTES // 4 if not args.hot_l2 else 4, dtype=torch.float32, device=device)
     # all work on one non-default stream (graph capture needs a non-default stream)
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)
@@ -414,6 +414,27 @@ def run_escs(args):
     lanes = [stream] + [torch.cuda.Stream(device) for _ in range(nstreams - 1)]
     groups = shard.partition_problems([d["flops"] for _, d in shard_problems], nstreams)
     owner = {i: g for g, idx in enumerate(groups) for i in idx}
+
+    # --group: each stream's problems go through ONE escs_spmm_group call (one
+    # launch per kernel instance, <= 32 problems each, instead of one per problem)
+    grouped = None
+    group_launches = len(shard_problems)
+    if args.group:
+        grouped = [escs.Group([shard_problems[i][1]["plan"] for i in idx],
+                              [shard_problems[i][1]["vals"] for i in idx],
+                              [shard_problems[i][1]["B"] for i in idx],
+                              [shard_problems[i][1]["C"] for i in idx]) for idx in groups]
+        group_launches = 0
+        for idx in groups:           # launches per call, as escs_spmm_group buckets them
+            keys = {}
+            for i in idx:
+                inf = shard_problems[i][1]["plan"].info
+                if inf["h"] == 1 and inf["variant"] == 1:
+                    key = (inf["bcols"], inf["colf"], inf["ufk"], inf["cta_warps"])
+                    keys[key] = keys.get(key, 0) + 1
+                else:
+                    group_launches += 1
+            group_launches += sum(-(-c // 32) for c in keys.values())
 
     def step(per_launch=None, serial=False):
         if serial:      # every launch on the timed stream (the 1-stream figure)
@@ -429,13 +450,17 @@ def run_escs(args):
             fork.record(stream)
             for s_ in lanes[1:]:
                 s_.wait_event(fork)
-        for i, (p, d) in enumerate(shard_problems):
-            st = lanes[owner[i]]
-            if per_launch is not None:
-                per_launch[i][0].record(st)
-            escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], st)
-            if per_launch is not None:
-                per_launch[i][1].record(st)
+        if grouped:
+            for g, st in zip(grouped, lanes):
+                g(stream=st)
+        else:
+            for i, (p, d) in enumerate(shard_problems):
+                st = lanes[owner[i]]
+                if per_launch is not None:
+                    per_launch[i][0].record(st)
+                escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], st)
+                if per_launch is not None:
+                    per_launch[i][1].record(st)
         for s_ in lanes[1:]:
             j = torch.cuda.Event()
             j.record(s_)
@@ -716,7 +741,9 @@ def run_escs(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "problems": len(problems), "sharding": sharding,
                        "streams": nstreams,
-                       "l2": "flushed before every step (256 MiB write); each problem touched once per step",
+                       "grouped": bool(args.group),
+                       "l2": ("flushed before every step (256 MiB write); each problem touched once per step"
+                              if not args.hot_l2 else "NOT flushed (--hot-l2 diagnostic, not a bench value)"),
                        "plans": ("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates)"
                                  if args.autotune else "parameter table (escs_plan defaults)"),
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}},
@@ -744,7 +771,7 @@ def run_escs(args):
                              "probe_ms_per_step": probe_ms / K,
                              "frac": probe_ms / float(kern_ms.sum()),
                              "what": "t_probe / t_kernel: escs_gather_probe runs the same item walk and B-row gathers without values or FMAs (measured gather ceiling of this plan)"}},
-            "gpu_launches": nprob * K,   # this rank's escs_spmm launches in the timed region
+            "gpu_launches": group_launches * K,   # this rank's kernel launches in the timed region
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -801,7 +828,11 @@ def main(argv=None):
     ap.add_argument("--workload", default="suite")
     ap.add_argument("--no-compare", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--hot-l2", action="store_true",
+                    help="diagnostic only: skip the L2 flush between steps (not a bench value)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--group", type=int, default=0,
+                    help="1: each stream's problems in one escs_spmm_group call (grouped launches)")
     ap.add_argument("--streams", type=int, default=4,
                     help="suite: run the independent problems on this many streams (LPT by flops)")
     ap.add_argument("--cases-out", default=None)

@@ -102,6 +102,29 @@ int escs_spmm(escs_plan_t plan, const float *vals, const float *B, float *C,
               void *stream);
 
 /*
+ * escs_spmm_group -- n independent SpMMs C[i] = A_i x B[i] (a layer suite,
+ * the experts of a layer, Q/K/V projections) in as few launches as possible:
+ * the problems whose plans select the same kernel instance (UFi = 1, vector
+ * lane map, 16-byte aligned B/C) run as one grid -- the concatenation of their
+ * CTA tiles, up to 32 problems per launch -- so small latency-bound layers
+ * share one launch, ramp and tail; any other problem is launched on its own.
+ * Each CTA tile computes exactly what escs_spmm computes for it: results are
+ * bitwise identical to n separate escs_spmm calls.
+ *   n       number of problems, >= 0 (0: no-op).
+ *   plans   HOST array of n device plans on the current device; a plan may
+ *           appear at most once (its fixup workspace is per plan).
+ *   vals, B, C   HOST arrays of n DEVICE pointers with escs_spmm's meaning,
+ *           layout and ownership per problem; no C[i] may alias another
+ *           problem's vals, B or C.
+ * Enqueue-only on `stream` (no host sync, no allocation, graph capturable:
+ * the per-problem operands travel in the kernel parameters).  The problem
+ * order inside a launch is unspecified.  Returns ESCS_OK, ESCS_ERR_ARG
+ * (naming the offending problem) or ESCS_ERR_CUDA.
+ */
+int escs_spmm_group(int32_t n, const escs_plan_t *plans, const float *const *vals,
+                    const float *const *B, float *const *C, void *stream);
+
+/*
  * escs_pack -- the value half of the paper's data transformation ("ANNZ":
  * the nonzeros re-stored in kernel traversal order, §3.3.3; built
  * once and reused across inference calls): packed[s] =

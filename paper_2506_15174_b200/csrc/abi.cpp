@@ -531,6 +531,34 @@ int escs_spmm(escs_plan_t plan, const float* vals, const float* B, float* C, voi
     return spmm_common(plan, vals, B, C, stream, false);
 }
 
+int escs_spmm_group(int32_t n, const escs_plan_t* plans, const float* const* vals,
+                    const float* const* B, float* const* C, void* stream) {
+    clear_error();
+    if (n < 0) return fail(ESCS_ERR_ARG, "n must be >= 0");
+    if (n == 0) return ESCS_OK;
+    if (!plans || !vals || !B || !C) return fail(ESCS_ERR_ARG, "NULL pointer array");
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(ESCS_ERR_CUDA, "cudaGetDevice failed");
+    std::vector<const escs::DevPlan*> dps(n);
+    for (int i = 0; i < n; i++) {
+        const escs_plan_t P = plans[i];
+        const std::string at = " (problem " + std::to_string(i) + ")";
+        if (!P || P->host_only) return fail(ESCS_ERR_ARG, "plan is NULL or host-only" + at);
+        if (P->device != dev)
+            return fail(ESCS_ERR_ARG, "current device differs from the plan's device" + at);
+        if (!B[i] || !C[i] || (!vals[i] && P->host.header[3] > 0))
+            return fail(ESCS_ERR_ARG, "vals, B and C must be non-NULL device pointers" + at);
+        for (int j = 0; j < i; j++)
+            if (plans[j] == P)
+                return fail(ESCS_ERR_ARG, "a plan appears twice in one group (shared workspace)" + at);
+        dps[i] = &P->dev;
+    }
+    int e = escs::launch_group(n, dps.data(), vals, B, C, stream, false);
+    if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
+                                          cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
 int escs_spmm_scatter(escs_plan_t plan, const float* vals, const float* B, float* const* dsts,
                       int32_t n_dst, int64_t row_offset, uint32_t flags, void* stream) {
     clear_error();

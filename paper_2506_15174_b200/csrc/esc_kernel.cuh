@@ -59,6 +59,7 @@ struct KParams {
     int n_extra, mc;                               // mc: extra[0] is a multicast address
     long long row_off;
     float* extra[kMaxScatter];
+    static constexpr bool kScatter = true;
 };
 
 // L2 cache policies: the plan and value streams are read once per call
@@ -259,8 +260,8 @@ __device__ __forceinline__ void get_vals(const Stage<H>& st, int buf, int s, flo
 // __shfl_sync (each sub-warp reads its own column).  Full batches run
 // unpredicated; the last partial batch of an item predicates its FMAs
 // (structural zeros are never multiplied).
-template <class Map, int U, bool PROBE>
-__device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sbase,
+template <class Map, int U, bool PROBE, class PP>
+__device__ __forceinline__ void walk1(const PP& p, int beg, int end, int sbase,
                                       float (&acc)[1][Map::F], int lane) {
     constexpr int F = Map::F, S = Map::S, US = U * S;
     static_assert(32 % US == 0, "UFK * sub-warps must divide 32");
@@ -336,8 +337,8 @@ __device__ __forceinline__ void walk1(const KParams& p, int beg, int end, int sb
 // slot_addr: this lane's value positions for a chunk (exclusive warp scan of
 // the popcounts, Reading R1 order) -- the slot-map loads for CSR-ordered
 // values, or the positions themselves when the values are pre-packed.
-template <int H>
-__device__ __forceinline__ int slot_addr(const KParams& p, int pk, int sbase, int lane,
+template <int H, class PP>
+__device__ __forceinline__ int slot_addr(const PP& p, int pk, int sbase, int lane,
                                          int (&sl)[H]) {
     const unsigned mask = (unsigned)pk >> kColBits;
     const unsigned lt = (1u << lane) - 1u;
@@ -356,14 +357,14 @@ __device__ __forceinline__ int slot_addr(const KParams& p, int pk, int sbase, in
     return sbase + total;
 }
 
-template <int H>
-__device__ __forceinline__ void load_vals(const KParams& p, const int (&sl)[H], float (&w)[H]) {
+template <int H, class PP>
+__device__ __forceinline__ void load_vals(const PP& p, const int (&sl)[H], float (&w)[H]) {
 #pragma unroll
     for (int r = 0; r < H; r++) w[r] = sl[r] >= 0 ? ld_stream_f(p.vals + sl[r]) : 0.f;
 }
 
-template <int H, class Map, int U, bool PROBE>
-__device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, int end, int sbase,
+template <int H, class Map, int U, bool PROBE, class PP>
+__device__ __forceinline__ void walk(const PP& p, Stage<H>& st, int beg, int end, int sbase,
                                      float (&acc)[H][Map::F], int lane) {
     constexpr int F = Map::F, S = Map::S, US = U * S;
     static_assert(32 % US == 0, "UFK * sub-warps must divide 32");
@@ -381,9 +382,9 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
 #pragma unroll
         for (int r = 0; r < H; r++) { w[r] = 0.f; slB[r] = -1; }
     } else {
-        sbase = slot_addr<H>(p, pkA, sbase, lane, slA);
-        sbase = slot_addr<H>(p, pkB, sbase, lane, slB);
-        load_vals<H>(p, slA, w);
+        sbase = slot_addr<H, PP>(p, pkA, sbase, lane, slA);
+        sbase = slot_addr<H, PP>(p, pkB, sbase, lane, slB);
+        load_vals<H, PP>(p, slA, w);
     }
     put_chunk<H>(st, 0, lane, pkA, w);
     __syncwarp();
@@ -393,8 +394,8 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
         const bool more = c0 + 32 < n;
         if (more) {
             if constexpr (!PROBE) {
-                load_vals<H>(p, slB, w);                        // chunk c+1
-                if (c0 + 64 < n) sbase = slot_addr<H>(p, pkC, sbase, lane, slB);   // chunk c+2
+                load_vals<H, PP>(p, slB, w);                        // chunk c+1
+                if (c0 + 64 < n) sbase = slot_addr<H, PP>(p, pkC, sbase, lane, slB);   // chunk c+2
             }
         }
         const int pkN = pkB;
@@ -439,18 +440,20 @@ __device__ __forceinline__ void walk(const KParams& p, Stage<H>& st, int beg, in
 
 // Row r of a panel tile is written by sub-warp r % S (after the sub-warp
 // reduction every sub-warp holds the totals).
-template <int H, class Map>
-__device__ __forceinline__ void store_rows(const KParams& p, int panel, const float (&a)[H][Map::F],
+template <int H, class Map, class PP>
+__device__ __forceinline__ void store_rows(const PP& p, int panel, const float (&a)[H][Map::F],
                                            int sub, int lj) {
 #pragma unroll
     for (int r = 0; r < H; r++) {
         const int row = panel * H + r;
         if ((r % Map::S) == sub && row < p.m) {
             if (p.C) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
-            for (int d = 0; d < p.n_extra; d++) {   // fused all-gather epilogue
-                float* q = p.extra[d] + (size_t)(p.row_off + row) * p.n;
-                if (p.mc) Map::store_mc(q, a[r], p.n, lj);
-                else Map::store(q, a[r], p.n, lj);
+            if constexpr (PP::kScatter) {
+                for (int d = 0; d < p.n_extra; d++) {   // fused all-gather epilogue
+                    float* q = p.extra[d] + (size_t)(p.row_off + row) * p.n;
+                    if (p.mc) Map::store_mc(q, a[r], p.n, lj);
+                    else Map::store(q, a[r], p.n, lj);
+                }
             }
         }
     }
@@ -468,13 +471,13 @@ __host__ __device__ constexpr int warp_smem_floats() {
 // the panel's items in this tile).  Every warp of the CTA calls this; the
 // __syncthreads below is reached by all of them when the tile needs a combine
 // (the flag is tile-uniform).
-template <int H, class Map, int U, bool PROBE>
-__device__ __forceinline__ void process_tile(const KParams& p, float* smem, int tile, int w,
-                                             int lane) {
+template <int H, class Map, int U, bool PROBE, class PP>
+__device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile, int w,
+                                             int lane, int W) {
     constexpr int F = Map::F, S = Map::S, NR = Map::L * Map::F;   // NR: floats per tile row
     constexpr int WS = warp_smem_floats<H, Map>();
     const int sub = lane / Map::L, lj = lane % Map::L;
-    const int slot = tile * (blockDim.x >> 5) + w;
+    const int slot = tile * W + w;
     const int aux = p.item_aux[slot];
     const int4 it = p.items[slot];   // independent of aux: both loads in flight together
     const bool active = (aux >> 16) & 1;
@@ -488,9 +491,9 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
     const int panel = it.x;
     if (active) {
         if constexpr (H == 1) {
-            walk1<Map, U, PROBE>(p, it.y, it.z, it.w, acc, lane);
+            walk1<Map, U, PROBE, PP>(p, it.y, it.z, it.w, acc, lane);
         } else {
-            walk<H, Map, U, PROBE>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y,
+            walk<H, Map, U, PROBE, PP>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y,
                                    it.z, it.w, acc, lane);
         }
         if constexpr (S > 1) {   // warp-level reduction of the sub-warps
@@ -518,7 +521,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
         const bool heavy = (aux >> 18) & 1;
         const int cnt = (aux >> 8) & 0xff, lead = aux & 0xff;
         if (!((aux >> 17) & 1)) {   // every panel of this tile has exactly one item here
-            if (active) store_rows<H, Map>(p, panel, acc, sub, lj);
+            if (active) store_rows<H, Map, PP>(p, panel, acc, sub, lj);
             return;
         }
         float* mine = smem + (size_t)w * WS;
@@ -535,7 +538,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
         __syncthreads();
         if (!active) return;
         if (cnt == 1 && !heavy) {
-            store_rows<H, Map>(p, panel, acc, sub, lj);
+            store_rows<H, Map, PP>(p, panel, acc, sub, lj);
             return;
         }
         if (w != lead) return;
@@ -557,7 +560,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
                     }
         }
         if (!heavy) {
-            store_rows<H, Map>(p, panel, acc, sub, lj);
+            store_rows<H, Map, PP>(p, panel, acc, sub, lj);
             return;
         }
         // heavy panel: its tiles combine through the global workspace
@@ -584,8 +587,9 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
 #pragma unroll
             for (int f = 0; f < F; f++) acc[r][f] = 0.f;
         // partials summed in tile order (deterministic); D tiles' loads in
-        // flight at once (the walk's registers are dead here)
-        constexpr int D = H * F <= 8 ? 4 : H * F <= 16 ? 2 : 1;
+        // flight at once (the walk's registers are dead here; fewer for UFi > 1,
+        // whose H x F accumulators would otherwise set the kernel's register count)
+        constexpr int D = H == 1 ? (F <= 16 ? 4 : 2) : (H * F <= 8 ? 4 : H * F <= 16 ? 2 : 1);
 #pragma unroll 1
         for (int t0 = 0; t0 < hv.z; t0 += D) {
             float q[D][H][F];
@@ -608,7 +612,7 @@ __device__ __forceinline__ void process_tile(const KParams& p, float* smem, int 
 #pragma unroll
                         for (int f = 0; f < F; f++) acc[r][f] += q[d][r][f];
         }
-        store_rows<H, Map>(p, hv.x, acc, sub, lj);
+        store_rows<H, Map, PP>(p, hv.x, acc, sub, lj);
         if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
     }
 }
@@ -621,10 +625,65 @@ template <int H, class Map, int U, bool PROBE>
 __global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_kernel(KParams p) {
     extern __shared__ __align__(16) float smem[];
     grid_dep_launch();   // the next launch may start reading its plan
-    process_tile<H, Map, U, PROBE>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31);
+    process_tile<H, Map, U, PROBE, KParams>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31,
+                                   blockDim.x >> 5);
 }
 
 using KernelFn = void (*)(KParams);
+
+// Grouped launch (escs_spmm_group): up to kMaxGroup independent problems
+// whose plans select the same kernel instance run as ONE grid -- the
+// concatenation of their CTA tiles -- so a suite of small, latency-bound
+// layers pays one launch and one ramp/tail instead of one per layer.  The
+// per-problem operands travel in the kernel's parameter space (no per-call
+// copy, graph capturable).  A CTA finds its problem by binary search over the
+// tile prefix; a problem whose tiles are narrower than the launch's block
+// (W < blockDim/32) leaves the extra warps idle (they still meet the tile's
+// combine barrier).  Each tile is processed exactly as by esc_spmm_kernel, so
+// results are bitwise identical to separate escs_spmm calls.
+constexpr int kMaxGroup = 32;
+struct GProb {
+    const int* gpk;
+    const int* slot;
+    const int4* items;
+    const int* item_aux;
+    const int2* tile_heavy;
+    const int4* heavy;
+    float* ws;
+    int* counters;
+    const float* vals;
+    const float* B;
+    float* C;
+    int m, n, W, packed;
+    static constexpr bool kScatter = false;   // no fused all-gather in grouped launches
+};
+struct GroupParams {
+    int n;
+    int tile_start[kMaxGroup + 1];
+    GProb prob[kMaxGroup];
+};
+
+template <int H, class Map, int U>
+__global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_group_kernel(const __grid_constant__ GroupParams gp) {
+    extern __shared__ __align__(16) float smem[];
+    grid_dep_launch();
+    const int t = blockIdx.x;
+    int lo = 0, hi = gp.n - 1;          // last problem with tile_start <= t
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (gp.tile_start[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const GProb& q = gp.prob[lo];       // read in place from the parameter space
+    const int tile = t - gp.tile_start[lo], w = threadIdx.x >> 5;
+    if (w >= q.W) {                     // idle warp: only the tile's combine barrier
+        if ((q.item_aux[tile * q.W] >> 17) & 1) __syncthreads();
+        return;
+    }
+    process_tile<H, Map, U, false, GProb>(q, smem, tile, w, threadIdx.x & 31, q.W);
+}
+
+using GroupFn = void (*)(GroupParams);
 
 }  // namespace kern
 }  // namespace escs

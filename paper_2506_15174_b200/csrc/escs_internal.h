@@ -69,6 +69,10 @@ struct DevPlan {
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
                 bool vec_ok, bool packed = false, float* const* extra = nullptr,
                 int n_extra = 0, long long row_off = 0, bool multicast = false);
+// escs_spmm_group: n independent SpMMs, grouped into one launch per kernel
+// instance (UFi = 1 vector plans; the rest launch one by one).
+int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
+                 const float* const* B, float* const* C, void* stream, bool packed);
 // escs_pack: packed[s] = vals[slot[s]].
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream);
 // Launch the gather probe (same walk, loads only).

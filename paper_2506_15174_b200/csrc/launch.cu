@@ -2,6 +2,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <utility>
+#include <vector>
 
 #include "esc_kernel.cuh"
 #include "escs_internal.h"
@@ -172,6 +175,87 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
     p.row_off = row_off;
     for (int d = 0; d < n_extra && d < kern::kMaxScatter; d++) p.extra[d] = extra[d];
     return launch(fn, dp, p, smem_for(dp, vec), stream);
+}
+
+int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
+                 const float* const* B, float* const* C, void* stream, bool packed) {
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+    // problems with a grouped instance (UFi = 1, vector map, aligned B/C),
+    // keyed by kernel; everything else launches on its own, in input order
+    std::vector<std::pair<kern::GroupFn, int>> keyed;
+    for (int i = 0; i < n; i++) {
+        const DevPlan& dp = *dps[i];
+        if (dp.n_tiles == 0) continue;
+        const bool vec = dp.variant == 1 && al16(B[i]) && al16(C[i]);
+        kern::GroupFn g = nullptr;
+        if (vec && dp.h == 1 && smem_for(dp, true) <= 48 * 1024)
+            g = kern::get_vec_group(dp.bcols, dp.colf > 0 ? dp.colf : kern::default_colf(dp.bcols),
+                                    dp.ufk);
+        if (!g) {
+            const int e = launch_spmm(dp, vals[i], B[i], C[i], stream, vec, packed);
+            if (e) return e;
+            continue;
+        }
+        keyed.emplace_back(g, i);
+    }
+    // one launch per (kernel, tile width): a CTA as wide as its problem's
+    // tiles (idle warps would hold registers and shared memory for nothing)
+    auto key = [&](const std::pair<kern::GroupFn, int>& x) {
+        return std::make_pair(reinterpret_cast<uintptr_t>(x.first), dps[x.second]->cta_warps);
+    };
+    std::stable_sort(keyed.begin(), keyed.end(),
+                     [&](const auto& a, const auto& b) { return key(a) < key(b); });
+    for (size_t a = 0; a < keyed.size();) {
+        size_t b = a;
+        while (b < keyed.size() && b - a < (size_t)kern::kMaxGroup && key(keyed[b]) == key(keyed[a])) b++;
+        kern::GroupParams gp = {};
+        gp.n = (int)(b - a);
+        int tiles = 0, maxw = 0;
+        size_t warp_smem = 0;
+        bool pdl = true;
+        for (size_t j = a; j < b; j++) {
+            const int i = keyed[j].second;
+            const DevPlan& dp = *dps[i];
+            kern::GProb& q = gp.prob[j - a];
+            q.gpk = dp.gpk;
+            q.slot = dp.slot;
+            q.items = reinterpret_cast<const int4*>(dp.items);
+            q.item_aux = dp.item_aux;
+            q.tile_heavy = reinterpret_cast<const int2*>(dp.tile_heavy);
+            q.heavy = reinterpret_cast<const int4*>(dp.heavy);
+            q.ws = dp.ws;
+            q.counters = dp.counters;
+            q.vals = vals[i];
+            q.B = B[i];
+            q.C = C[i];
+            q.m = dp.m;
+            q.n = dp.bcols;
+            q.W = dp.cta_warps;
+            q.packed = packed ? 1 : 0;
+            gp.tile_start[j - a] = tiles;
+            tiles += dp.n_tiles;
+            maxw = std::max(maxw, dp.cta_warps);
+            warp_smem = std::max(warp_smem, smem_for(dp, true) / dp.cta_warps);
+            pdl = pdl && dp.pdl;
+        }
+        gp.tile_start[gp.n] = tiles;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(tiles);
+        cfg.blockDim = dim3(32 * maxw);
+        cfg.dynamicSmemBytes = warp_smem * maxw;
+        cfg.stream = (cudaStream_t)stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, keyed[a].first, gp);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return (int)e;
+        a = b;
+    }
+    return 0;
 }
 
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok) {

@@ -22,7 +22,7 @@ PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "s
                "item_panel", "item_group_begin", "item_gcol_ptr")
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
                     "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
-                    "escs_pack", "escs_spmm_packed", "escs_spmm_scatter")
+                    "escs_pack", "escs_spmm_packed", "escs_spmm_scatter", "escs_spmm_group")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -62,6 +62,9 @@ _lib.escs_plan_ex.restype = _vp
 _lib.escs_spmm.argtypes = [_vp, _vp, _vp, _vp, _vp]
 _lib.escs_spmm.restype = ctypes.c_int
 _lib.escs_spmm_packed.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.escs_spmm_group.restype = _i32
+_lib.escs_spmm_group.argtypes = [_i32, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p),
+                                 ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _vp]
 _lib.escs_spmm_packed.restype = ctypes.c_int
 _lib.escs_spmm_scatter.argtypes = [_vp, _vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i32, _i64,
                                    ctypes.c_uint32, _vp]
@@ -190,6 +193,42 @@ def escs_spmm(plan: Plan, vals, B, C, stream=None) -> None:
     rc = _lib.escs_spmm(plan.handle, _ptr(vals), _ptr(B), _ptr(C), _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
+
+
+class Group:
+    """Marshalled argument arrays of one escs_spmm_group call (built once,
+    reused every call: the C ABI reads them on the host at enqueue time)."""
+
+    def __init__(self, plans, vals, B, C):
+        n = len(plans)
+        if not (len(vals) == len(B) == len(C) == n):
+            raise EscsError(ESCS_ERR_ARG, "plans, vals, B and C must have the same length")
+        for pl, v, b, c in zip(plans, vals, B, C):
+            for t in (v, b, c):
+                if t is not None and not isinstance(t, int):
+                    if not t.is_cuda or t.dtype.itemsize != 4 or not t.is_contiguous():
+                        raise EscsError(ESCS_ERR_ARG, "vals, B, C must be contiguous fp32 CUDA tensors")
+            if not isinstance(b, int) and b.numel() != pl.k * pl.bcols:
+                raise EscsError(ESCS_ERR_ARG, f"B must have k*bCols = {pl.k * pl.bcols} elements")
+            if not isinstance(c, int) and c.numel() != pl.m * pl.bcols:
+                raise EscsError(ESCS_ERR_ARG, f"C must have m*bCols = {pl.m * pl.bcols} elements")
+        arr = lambda xs: (ctypes.c_void_p * max(n, 1))(*[_ptr(x) for x in xs])
+        self.n = n
+        self.keep = (list(plans), list(vals), list(B), list(C))   # keep tensors alive
+        self.plans = (ctypes.c_void_p * max(n, 1))(*[pl.handle for pl in plans])
+        self.vals, self.B, self.C = arr(vals), arr(B), arr(C)
+
+    def __call__(self, stream=None) -> None:
+        rc = _lib.escs_spmm_group(self.n, self.plans, self.vals, self.B, self.C,
+                                  _stream_ptr(stream))
+        if rc != ESCS_OK:
+            _raise_last()
+
+
+def escs_spmm_group(plans, vals, B, C, stream=None) -> None:
+    """C[i] = A_i x B[i] for independent problems, grouped into as few
+    launches as possible (bitwise identical to separate escs_spmm calls)."""
+    Group(plans, vals, B, C)(stream)
 
 
 def escs_pack(plan: Plan, vals, packed, stream=None) -> None:

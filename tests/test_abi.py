@@ -120,3 +120,14 @@ def test_params_out_of_range_rejected():
         pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **ok)
         assert pl.info["tile_order"] in (1, 2)
         pl.close()
+
+
+def test_group_arg_errors_without_gpu():
+    lib = ctypes.CDLL(escs.LIB_PATH)
+    lib.escs_spmm_group.restype = ctypes.c_int32
+    lib.escs_spmm_group.argtypes = [ctypes.c_int32] + [ctypes.c_void_p] * 5
+    assert lib.escs_spmm_group(0, None, None, None, None, None) == escs.ESCS_OK
+    assert lib.escs_spmm_group(-1, None, None, None, None, None) == escs.ESCS_ERR_ARG
+    assert lib.escs_spmm_group(2, None, None, None, None, None) == escs.ESCS_ERR_ARG
+    code, msg = escs.escs_last_error()
+    assert code == escs.ESCS_ERR_ARG and "NULL" in msg

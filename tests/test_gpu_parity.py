@@ -421,3 +421,83 @@ def test_tile_order_exact(torch_cuda, order, warps):
     C, pl = run_escs(torch_cuda, A, B, ufi=1, T=24, cta_warps=warps, tile_order=order)
     assert pl.info["tile_order"] == order
     check_exact(A, B, C)
+
+
+def _group_case(torch, problems, params, graph=False):
+    """escs_spmm_group over `problems` (list of (A, B)) with per-problem plan
+    parameters vs one escs_spmm per problem: bitwise equal, and (dyadic
+    inputs) equal to the oracle."""
+    from paper_2506_15174_b200 import escs
+    plans, dv, dB, dCg, dCs = [], [], [], [], []
+    for (A, B), prm in zip(problems, params):
+        n = B.shape[1]
+        plans.append(escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, **prm))
+        dv.append(torch.from_numpy(A.vals).cuda() if A.nnz else torch.zeros(1, device="cuda"))
+        dB.append(torch.from_numpy(np.ascontiguousarray(B)).cuda())
+        dCg.append(torch.full((A.m, n), float("nan"), device="cuda"))
+        dCs.append(torch.full((A.m, n), float("nan"), device="cuda"))
+    for pl, v, b, c in zip(plans, dv, dB, dCs):
+        escs.escs_spmm(pl, v, b, c)
+    grp = escs.Group(plans, dv, dB, dCg)
+    if graph:
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            grp(stream=s)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                grp(stream=s)
+        for c in dCg:
+            c.fill_(float("nan"))
+        g.replay()
+        g.replay()
+    else:
+        grp()
+        grp()      # heavy-panel counters self-reset between calls
+    torch.cuda.synchronize()
+    for (A, B), cg, cs in zip(problems, dCg, dCs):
+        assert torch.equal(cg, cs)
+        check_exact(A, B, cg.cpu().numpy())
+    return [pl.info for pl in plans]
+
+
+def test_group_mixed_suite_bitwise(torch_cuda):
+    """Grouped launch over a mixed suite: bCols 32/64/128 (several kernel
+    instances), UFi 1 and 4 (the latter launched singly), different tile
+    widths and lane maps in one launch (idle warps), heavy panels, ragged m,
+    an empty matrix; more than 32 problems of one instance (chunked)."""
+    problems, params = [], []
+    for i, (m, k, s) in enumerate([(512, 512, 0.7), (2048, 512, 0.9), (256, 2304, 0.95),
+                                   (512, 2048, 0.98), (130, 257, 0.8)]):
+        A0 = synth.magnitude_pruned(m, k, s, 300 + i)
+        for n in (32, 64, 128):
+            problems.append(synth.dyadic_twin(A0, n, 7 * i + n))
+            params.append({"autotune": 1})
+    A0 = synth.power_law(4096, 4096, 0.99, 5)
+    problems.append(synth.dyadic_twin(A0, 128, 11))
+    params.append({"ufi": 1, "T": 32, "cta_warps": 4})                 # heavy panels
+    A0 = synth.random_csr(130, 257, 9000, 4, empty_rows=(3, 64, 65), dense_rows=(9,))
+    problems.append(synth.dyadic_twin(A0, 64, 12))
+    params.append({"ufi": 4, "T": 16, "cta_warps": 8})                 # UFi 4: single launch
+    problems.append(synth.dyadic_twin(synth.random_csr(37, 50, 0, 1), 32, 13))
+    params.append({})                                                  # nnz = 0
+    for j in range(34):                                                # > kMaxGroup, one instance
+        A0 = synth.random_csr(33 + j, 70, 300 + 13 * j, 400 + j)
+        problems.append(synth.dyadic_twin(A0, 64, 500 + j))
+        params.append({"ufi": 1, "T": 8 + j, "cta_warps": 1 + j % 16, "ufk": 4, "colf": 4})
+    infos = _group_case(torch_cuda, problems, params)
+    assert any(i["n_heavy"] > 0 for i in infos)
+    assert len({i["cta_warps"] for i in infos}) > 3
+
+
+def test_group_graph_capture(torch_cuda):
+    problems, params = [], []
+    for i, s in enumerate((0.7, 0.9, 0.98)):
+        A0 = synth.magnitude_pruned(512, 512, s, 600 + i)
+        for n in (32, 128):
+            problems.append(synth.dyadic_twin(A0, n, 610 + i + n))
+            params.append({})
+    A0 = synth.power_law(4096, 4096, 0.99, 5)
+    problems.append(synth.dyadic_twin(A0, 128, 11))
+    params.append({"ufi": 1, "T": 32, "cta_warps": 4})
+    _group_case(torch_cuda, problems, params, graph=True)
