@@ -18,7 +18,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "escs_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# ESCS_ORACLE_LIB: a prebuilt oracle library to load instead (tests/test_oracle_mutants.py
+# points it at deliberately broken copies to show the pins catch them)
+_LIB_OVERRIDE = os.environ.get("ESCS_ORACLE_LIB")
+_LIB = _LIB_OVERRIDE or os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -28,6 +31,8 @@ PLAN_HEADER_FIELDS = ("version", "m", "k", "nnz", "bCols", "h", "T",
 
 def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc (-O2, OpenMP over rows only)."""
+    if _LIB_OVERRIDE:
+        return _LIB
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared",
