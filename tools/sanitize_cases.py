@@ -1,6 +1,8 @@
 """Small escs_spmm cases for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): UFi 1 and 4, vector and scalar lane maps, split and
-heavy panels, empty panels, ragged last panel.  Exits non-zero on a mismatch.
+heavy panels, empty panels, ragged last panel, long UFi > 1 items (operand
+pipeline), pre-packed values, a grouped launch, the scatter epilogue.  Exits
+non-zero on a mismatch.
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
 """
@@ -28,6 +30,10 @@ def main():
         cases.append((P, n, dict(ufi=1, T=16, cta_warps=2, colf=colf)))
     for n in (4, 8, 16):                                               # narrow-B sub-warp maps
         cases.append((A0, n, dict(ufi=1, T=7, cta_warps=3)))
+    W = synth.random_csr(61, 3000, 40000, 2, empty_rows=(4,), dense_rows=(7,))
+    for ufi in (2, 3, 4):               # long items: the UFi > 1 three-chunk operand pipeline
+        cases.append((W, 128, dict(ufi=ufi, T=300, cta_warps=4)))
+        cases.append((W, 32, dict(ufi=ufi, T=130, cta_warps=2)))
     bad = 0
     for A, n, prm in cases:
         Ad, B = synth.dyadic_twin(A, n, 7)
@@ -39,6 +45,36 @@ def main():
         ok = np.array_equal(C.cpu().numpy().astype(np.float64), ref)
         print(n, prm, "ok" if ok else "MISMATCH", flush=True)
         bad += not ok
+    # values pre-packed by escs_pack (the paper's ANNZ), UFi 4, long items
+    Ad, B = synth.dyadic_twin(W, 64, 8)
+    pl = escs.escs_plan_ex(W.m, W.k, W.nnz, W.rowptr, W.colidx, 64, ufi=4, T=300, cta_warps=4)
+    dv = torch.from_numpy(Ad.vals).cuda()
+    pk = torch.empty_like(dv)
+    C = torch.empty(W.m, 64, device="cuda")
+    escs.escs_pack(pl, dv, pk)
+    escs.escs_spmm_packed(pl, pk, torch.from_numpy(B).cuda(), C)
+    torch.cuda.synchronize()
+    ok = np.array_equal(C.cpu().numpy().astype(np.float64),
+                        oracle.spmm(W.m, W.k, W.rowptr, W.colidx, Ad.vals, B))
+    print("packed", "ok" if ok else "MISMATCH", flush=True)
+    bad += not ok
+    # grouped launch: mixed tile widths (idle warps), heavy panels, a UFi-4 single
+    probs = [(A0, 64, dict(ufi=1, T=7, cta_warps=3)), (P, 64, dict(ufi=1, T=16, cta_warps=2)),
+             (A0, 64, dict(ufi=1, T=9, cta_warps=5)), (W, 64, dict(ufi=4, T=300, cta_warps=4)),
+             (P, 128, dict(ufi=1, T=16, cta_warps=2))]
+    plans, vs, Bs, Cs, refs = [], [], [], [], []
+    for j, (A, n, prm) in enumerate(probs):
+        Ad, B = synth.dyadic_twin(A, n, 20 + j)
+        plans.append(escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, **prm))
+        vs.append(torch.from_numpy(Ad.vals).cuda())
+        Bs.append(torch.from_numpy(B).cuda())
+        Cs.append(torch.empty(A.m, n, device="cuda"))
+        refs.append(oracle.spmm(A.m, A.k, A.rowptr, A.colidx, Ad.vals, B))
+    escs.escs_spmm_group(plans, vs, Bs, Cs)
+    torch.cuda.synchronize()
+    ok = all(np.array_equal(c.cpu().numpy().astype(np.float64), r) for c, r in zip(Cs, refs))
+    print("group", "ok" if ok else "MISMATCH", flush=True)
+    bad += not ok
     # fused all-gather epilogue: two row blocks into two destinations
     A, n = A0, 128
     Ad, B = synth.dyadic_twin(A, n, 9)
