@@ -1,6 +1,7 @@
 /* Plain-C client of libescs.so (include/escs.h): no Python, no torch.
  *   abi_client host   -- host-only plan + export + error codes (no GPU)
- *   abi_client device -- plan, escs_spmm on cudaMalloc'd buffers, check C
+ *   abi_client device -- plan, escs_spmm and escs_spmm_group on cudaMalloc'd
+ *                        buffers, check C
  * The matrix is the 4x4 worked example of SPEC.md S:123 (golden plan in
  * tests/golden/spec_4x4_plan.json); C = A x B is checked exactly against a
  * hand-computed product.  Exit code 0 = pass. */
@@ -53,6 +54,25 @@ static int check_device(void) {
     if (escs_spmm(pl, dv, dB, dC, NULL) != ESCS_OK) return 12;
     if (cudaMemcpy(C, dC, sizeof C, cudaMemcpyDeviceToHost) != cudaSuccess) return 13;
     if (memcmp(C, ref, sizeof C)) return 14;                       /* small integers: exact */
+    /* escs_spmm_group: the same problem twice (two plans, two outputs), one call */
+    escs_plan_t pl2 = escs_plan(4, 4, 7, rowptr, colidx, n);
+    float* dC2;
+    if (!pl2 || cudaMalloc((void**)&dC2, sizeof C)) return 15;
+    cudaMemset(dC, 0xff, sizeof C);
+    cudaMemset(dC2, 0xff, sizeof C);
+    escs_plan_t plans[2] = {pl, pl2};
+    const float* vs[2] = {dv, dv};
+    const float* Bs[2] = {dB, dB};
+    float* Cs[2] = {dC, dC2};
+    if (escs_spmm_group(2, plans, vs, Bs, Cs, NULL) != ESCS_OK) return 16;
+    escs_plan_t same[2] = {pl, pl};
+    if (escs_spmm_group(2, same, vs, Bs, Cs, NULL) != ESCS_ERR_ARG) return 17;  /* plan twice */
+    for (int o = 0; o < 2; o++) {
+        if (cudaMemcpy(C, Cs[o], sizeof C, cudaMemcpyDeviceToHost) != cudaSuccess) return 18;
+        if (memcmp(C, ref, sizeof C)) return 19;
+    }
+    escs_free(pl2);
+    cudaFree(dC2);
     escs_free(pl);
     cudaFree(dv); cudaFree(dB); cudaFree(dC);
     printf("device ok\n");
