@@ -501,3 +501,43 @@ def test_group_graph_capture(torch_cuda):
     problems.append(synth.dyadic_twin(A0, 128, 11))
     params.append({"ufi": 1, "T": 32, "cta_warps": 4})
     _group_case(torch_cuda, problems, params, graph=True)
+
+
+def test_suite_bench_launch_configuration(torch_cuda):
+    """The whole default bench step as bench.py times it: configs[1]+[2]
+    (90 layers), autotuned plans, layers LPT-partitioned over 4 streams forked
+    from / joined into one stream, PDL chains on each, repeated; every C is
+    bitwise equal to a one-stream run and within the G2 gate of the oracle."""
+    torch = torch_cuda
+    from paper_2506_15174_b200 import escs, shard
+    probs = synth.suite()
+    dev = []
+    for p in probs:
+        A = p.A
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=1)
+        dev.append((pl, torch.from_numpy(A.vals).cuda(), torch.from_numpy(p.B).cuda(),
+                    torch.full((A.m, p.bcols), float("nan"), device="cuda"),
+                    torch.full((A.m, p.bcols), float("nan"), device="cuda")))
+    main = torch.cuda.Stream()
+    lanes = [main] + [torch.cuda.Stream() for _ in range(3)]
+    groups = shard.partition_problems([2 * p.A.nnz * p.bcols for p in probs], 4)
+    for _ in range(3):
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for s in lanes[1:]:
+            s.wait_event(fork)
+        for g, s in zip(groups, lanes):
+            for i in g:
+                pl, v, b, c, _ = dev[i]
+                escs.escs_spmm(pl, v, b, c, stream=s)
+        for s in lanes[1:]:
+            j = torch.cuda.Event()
+            j.record(s)
+            main.wait_event(j)
+    for pl, v, b, _, c1 in dev:
+        escs.escs_spmm(pl, v, b, c1, stream=main)
+    torch.cuda.synchronize()
+    for p, (_, _, _, c4, c1) in zip(probs, dev):
+        assert torch.equal(c4, c1), p.name
+    for p, (_, _, _, c4, _) in list(zip(probs, dev))[::9]:
+        check_tol(p.A, p.B, c4.cpu().numpy())
