@@ -377,6 +377,7 @@ def run_escs(args):
         mine = list(range(len(problems)))
         sharding = f"row-block x{world}"
     dev = {"_device": device}
+    want_tp = bool(args.autotune and args.tp_plans and args.streams > 1 and len(mine) > 1)
     shard_problems = []
     plan_s = 0.0
     plan_info = []
@@ -389,10 +390,19 @@ def run_escs(args):
             pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, **tune)
         else:
             A, pl = shard.plan_shard(p.A, p.bcols, world, rank, **tune)
+        # throughput-objective plans (autotune = 2) for the multi-stream step:
+        # the latency-tuned plan of a layer alone tends to fill every SM, which
+        # starves the layers co-running on the other streams
+        pl_tp = None
+        if want_tp:
+            if mode == "problems":
+                pl_tp = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=2)
+            else:
+                pl_tp = shard.plan_shard(p.A, p.bcols, world, rank, autotune=2)[1]
         plan_s += time.perf_counter() - t0
         info = pl.info
         plan_info.append(info)
-        d = {"plan": pl, "A": A,
+        d = {"plan": pl, "plan_tp": pl_tp or pl, "A": A,
              "vals": torch.from_numpy(A.vals).to(device) if A.nnz else torch.zeros(1, device=device),
              "B": torch.from_numpy(p.B).to(device),
              "C": torch.empty((A.m, p.bcols), dtype=torch.float32, device=device),
@@ -420,7 +430,7 @@ def run_escs(args):
     grouped = None
     group_launches = len(shard_problems)
     if args.group:
-        grouped = [escs.Group([shard_problems[i][1]["plan"] for i in idx],
+        grouped = [escs.Group([shard_problems[i][1]["plan_tp"] for i in idx],
                               [shard_problems[i][1]["vals"] for i in idx],
                               [shard_problems[i][1]["B"] for i in idx],
                               [shard_problems[i][1]["C"] for i in idx]) for idx in groups]
@@ -428,7 +438,7 @@ def run_escs(args):
         for idx in groups:           # launches per call, as escs_spmm_group buckets them
             keys = {}
             for i in idx:
-                inf = shard_problems[i][1]["plan"].info
+                inf = shard_problems[i][1]["plan_tp"].info
                 if inf["h"] == 1 and inf["variant"] == 1:
                     key = (inf["bcols"], inf["colf"], inf["ufk"], inf["cta_warps"])
                     keys[key] = keys.get(key, 0) + 1
@@ -458,7 +468,7 @@ def run_escs(args):
                 st = lanes[owner[i]]
                 if per_launch is not None:
                     per_launch[i][0].record(st)
-                escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], st)
+                escs.escs_spmm(d["plan_tp"], d["vals"], d["B"], d["C"], st)
                 if per_launch is not None:
                     per_launch[i][1].record(st)
         for s_ in lanes[1:]:
@@ -744,7 +754,10 @@ def run_escs(args):
                        "grouped": bool(args.group),
                        "l2": ("flushed before every step (256 MiB write); each problem touched once per step"
                               if not args.hot_l2 else "NOT flushed (--hot-l2 diagnostic, not a bench value)"),
-                       "plans": ("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates)"
+                       "plans": (("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates); "
+                                  + ("the multi-stream step (value) runs throughput-objective plans (autotune=2: candidates "
+                                     "timed as 4 concurrent copies on 4 streams), serial / per-launch / per-case figures "
+                                     "the latency-objective plans (autotune=1)" if want_tp else "latency objective (autotune=1)"))
                                  if args.autotune else "parameter table (escs_plan defaults)"),
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}},
             "roofline": {"bound": "hbm", "achieved": step_bytes_per_s, "peak": hbm, "unit": "GB/s",
@@ -836,6 +849,8 @@ def main(argv=None):
     ap.add_argument("--streams", type=int, default=4,
                     help="suite: run the independent problems on this many streams (LPT by flops)")
     ap.add_argument("--cases-out", default=None)
+    ap.add_argument("--no-tp-plans", dest="tp_plans", action="store_false",
+                    help="run the multi-stream step on the latency-tuned plans too (no autotune=2 plans)")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table only (default: plan-time autotuning)")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],

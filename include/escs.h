@@ -199,7 +199,14 @@ typedef struct {
                              parameters given explicitly are not searched.
                              Adds a few ms to escs_plan; the plan arrays are
                              still the canonical plan of the chosen (UFi, T).
-                             Also enabled by ESCS_AUTOTUNE=1.                  */
+                             Also enabled by ESCS_AUTOTUNE=1.
+                             2: same search, throughput objective: each
+                             candidate is timed as 4 concurrent chains of
+                             its launches on 4 streams (each with its own
+                             fixup workspace; for callers that overlap
+                             independent SpMMs on several streams; prefers
+                             plans that leave SMs to the other streams).
+                             Any other value: ESCS_ERR_ARG.                   */
     int32_t colf;         /* B columns per lane of the vector kernel: the bCols
                              coarsening factor (register tile of B columns,
                              §3.4).  0 = default (4; 8 at bCols 256); 8 or 16

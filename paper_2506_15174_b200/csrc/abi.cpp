@@ -337,12 +337,40 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // matrix and bCols.  Coordinate descent over the item size T (with the auto
 // tile width), then the tile width W, then UFk; every candidate is a complete
 // canonical plan, timed as back-to-back launches (min over 3 batches of 8).
+// Throughput objective (autotune = 2): kTuneStreams copies of a candidate
+// plan (each with its own workspace/counters and C) run concurrently, one per
+// stream, as independent layers of a suite would.
+constexpr int kTuneStreams = 4;
 struct TuneBufs {
     float *vals = nullptr, *B = nullptr, *C = nullptr;
+    float* Cx[kTuneStreams] = {};
     cudaStream_t stream = nullptr;
+    cudaStream_t sx[kTuneStreams] = {};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t ex[kTuneStreams] = {};
+    // per-stream heavy-panel workspace + counters for the concurrent copies
+    // (zeroed once; every launch leaves its counters at zero again)
+    float* wsx[kTuneStreams] = {};
+    int32_t* cntx[kTuneStreams] = {};
+    size_t ws_cap = 0, cnt_cap = 0;
+    bool scratch(size_t ws_elems, size_t n_cnt) {
+        if (ws_elems <= ws_cap && n_cnt <= cnt_cap) return true;
+        cudaDeviceSynchronize();
+        ws_cap = std::max(ws_cap, ws_elems);
+        cnt_cap = std::max(cnt_cap, n_cnt);
+        for (int i = 0; i < kTuneStreams; i++) {
+            if (wsx[i]) cudaFree(wsx[i]);
+            if (cntx[i]) cudaFree(cntx[i]);
+            wsx[i] = nullptr; cntx[i] = nullptr;
+            if (cudaMalloc(&wsx[i], ws_cap * 4) != cudaSuccess ||
+                cudaMalloc(&cntx[i], cnt_cap * 4) != cudaSuccess ||
+                cudaMemset(cntx[i], 0, cnt_cap * 4) != cudaSuccess)
+                return false;
+        }
+        return cudaDeviceSynchronize() == cudaSuccess;
+    }
     bool ok = false;
-    TuneBufs(int64_t m, int64_t k, int64_t nnz, int32_t n) {
+    TuneBufs(int64_t m, int64_t k, int64_t nnz, int32_t n, bool concurrent) {
         ok = cudaMalloc(&vals, std::max<int64_t>(nnz, 1) * 4) == cudaSuccess &&
              cudaMalloc(&B, (size_t)k * n * 4) == cudaSuccess &&
              cudaMalloc(&C, (size_t)m * n * 4) == cudaSuccess &&
@@ -350,6 +378,10 @@ struct TuneBufs {
              cudaMemset(B, 0, (size_t)k * n * 4) == cudaSuccess &&
              cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+        for (int i = 0; ok && concurrent && i < kTuneStreams; i++)
+            ok = cudaMalloc(&Cx[i], (size_t)m * n * 4) == cudaSuccess &&
+                 cudaStreamCreateWithFlags(&sx[i], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming) == cudaSuccess;
     }
     ~TuneBufs() {
         if (vals) cudaFree(vals);
@@ -358,6 +390,13 @@ struct TuneBufs {
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (stream) cudaStreamDestroy(stream);
+        for (int i = 0; i < kTuneStreams; i++) {
+            if (Cx[i]) cudaFree(Cx[i]);
+            if (sx[i]) cudaStreamDestroy(sx[i]);
+            if (ex[i]) cudaEventDestroy(ex[i]);
+            if (wsx[i]) cudaFree(wsx[i]);
+            if (cntx[i]) cudaFree(cntx[i]);
+        }
         cudaGetLastError();
     }
 };
@@ -382,22 +421,69 @@ float time_plan(escs_plan_t P, TuneBufs& b) {
     return best;
 }
 
+// Throughput objective: the copies run one per stream, each stream a chain of
+// kBatch launches, all released together after the busy-wait; time per
+// launch = span / (kBatch * copies).
+float time_plans_concurrent(escs_plan_t P0, TuneBufs& b) {
+    float best = 1e30f;
+    const bool vec = aligned16(b.B) && aligned16(b.C);
+    // the copies share the read-only plan arrays; each has its own workspace
+    // and counters (one plan must not run on two streams at once)
+    escs::DevPlan dp[kTuneStreams];
+    const auto& ph = P0->host;
+    if (!b.scratch((size_t)ph.n_heavy_tiles * P0->dev.h * P0->dev.bcols, (size_t)ph.n_heavy))
+        return 1e30f;
+    for (int i = 0; i < kTuneStreams; i++) {
+        dp[i] = P0->dev;
+        dp[i].ws = b.wsx[i];
+        dp[i].counters = b.cntx[i];
+    }
+    const escs::DevPlan* P[kTuneStreams];
+    for (int i = 0; i < kTuneStreams; i++) P[i] = &dp[i];
+    for (int i = 0; i < kTuneStreams; i++)
+        for (int w = 0; w < 2; w++) escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
+    constexpr int kBatch = 8;
+    for (int rep = 0; rep < 3; rep++) {
+        escs::launch_spin(b.stream, 200000);
+        cudaEventRecord(b.e0, b.stream);
+        for (int i = 0; i < kTuneStreams; i++) cudaStreamWaitEvent(b.sx[i], b.e0, 0);
+        for (int j = 0; j < kBatch; j++)
+            for (int i = 0; i < kTuneStreams; i++)
+                escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
+        for (int i = 0; i < kTuneStreams; i++) {
+            cudaEventRecord(b.ex[i], b.sx[i]);
+            cudaStreamWaitEvent(b.stream, b.ex[i], 0);
+        }
+        cudaEventRecord(b.e1, b.stream);
+        if (cudaEventSynchronize(b.e1) != cudaSuccess) return 1e30f;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, b.e0, b.e1);
+        best = std::min(best, ms / (kBatch * kTuneStreams));
+    }
+    return best;
+}
+
 escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                                 const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     escs_params q = ep ? *ep : escs_params{};
+    const bool concurrent = q.autotune == 2;
     q.autotune = 0;
     escs_plan_t best = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
     if (!best || nnz > 8000000) return best;   // large problems: many waves, heuristic holds
-    TuneBufs bufs(m, k, nnz, bCols);
+    TuneBufs bufs(m, k, nnz, bCols, concurrent);
     if (!bufs.ok) return best;
-    float tb = time_plan(best, bufs);
+    // a candidate's time under the chosen objective
+    auto timed = [&](escs_plan_t P) -> float {
+        return concurrent ? time_plans_concurrent(P, bufs) : time_plan(P, bufs);
+    };
+    float tb = timed(best);
     auto consider = [&](escs_params c) {
         escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
         if (!P) {
             clear_error();
             return;
         }
-        const float t = time_plan(P, bufs);
+        const float t = timed(P);
         if (t < tb) {
             escs_free(best);
             best = P;
@@ -426,10 +512,14 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             consider(c);
         }
     }
-    // stage 2: tile width
+    // stage 2: tile width.  Whole panels are packed per tile, so W sets both
+    // the warps per CTA and the tile count; the intermediate widths let a
+    // layer land on one full wave of the 148 SMs (2048x512@70% b128: 14 warps
+    // -> 147 tiles, 9.4 us vs 10.2 us at 16 warps -> 128 tiles; gpurun
+    // wave_sweep, profiles/r1_notes.md)
     if (!(ep && ep->cta_warps)) {
         const int W0 = best->params.cta_warps, T = best->params.T;
-        for (int W : {4, 8, 16}) {
+        for (int W : {4, 6, 8, 10, 12, 14, 16}) {
             if (W == W0) continue;
             escs_params c = q;
             c.ufi = h;
@@ -489,6 +579,10 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
 escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                       const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     const char* env = std::getenv("ESCS_AUTOTUNE");
+    if (ep && (ep->autotune < 0 || ep->autotune > 2)) {
+        fail(ESCS_ERR_ARG, "autotune must be 0 (off), 1 (latency) or 2 (concurrent throughput)");
+        return nullptr;
+    }
     const bool tune = (ep && ep->autotune) || (env && env[0] == '1');
     if (!tune || (ep && ep->host_only)) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, ep);
     return make_plan_autotuned(m, k, nnz, rowptr, colidx, bCols, ep);

@@ -112,7 +112,8 @@ def test_params_out_of_range_rejected():
     import pytest
     from paper_2506_15174_b200 import escs, synth
     A = synth.random_csr(20, 30, 100, 1)
-    for bad in ({"colf": 5}, {"tile_order": 3}, {"cta_warps": 17}, {"variant": 3}):
+    for bad in ({"colf": 5}, {"tile_order": 3}, {"cta_warps": 17}, {"variant": 3},
+                {"autotune": 3}, {"autotune": -1}):
         with pytest.raises(escs.EscsError) as e:
             escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **bad)
         assert e.value.code == escs.ESCS_ERR_ARG

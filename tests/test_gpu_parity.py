@@ -312,6 +312,32 @@ def test_autotuned_plan_parity(torch_cuda):
     check_exact(A, B, C)
 
 
+@pytest.mark.parametrize("shape", [(512, 2048, 0.7, 128), (2048, 512, 0.9, 32)])
+def test_throughput_tuned_plan_parity(torch_cuda, shape):
+    """autotune = 2 (candidates timed as 4 concurrent copies on 4 streams, the
+    plans bench.py's multi-stream step runs): still the canonical plan of its
+    (UFi, T), exact on the dyadic twin, and the tuning left the shared
+    workspace/counters of the returned plan clean (two calls, same result)."""
+    from paper_2506_15174_b200 import escs
+    m, k, s, n = shape
+    A0 = synth.magnitude_pruned(m, k, s, 43)
+    A, B = synth.dyadic_twin(A0, n, 44)
+    C, pl = run_escs(torch_cuda, A, B, autotune=2)
+    info = pl.info
+    assert info["autotuned"] == 1
+    got = pl.export()
+    ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, info["h"], info["T"], bCols=n)
+    for nm in oracle.PLAN_ARRAYS:
+        assert np.array_equal(got[nm], ref[nm]), nm
+    check_exact(A, B, C)
+    dv = torch_cuda.from_numpy(A.vals).cuda()
+    dB = torch_cuda.from_numpy(np.ascontiguousarray(B)).cuda()
+    dC = torch_cuda.empty((A.m, n), device="cuda")
+    escs.escs_spmm(pl, dv, dB, dC)
+    torch_cuda.cuda.synchronize()
+    assert np.array_equal(dC.cpu().numpy(), C)
+
+
 def test_dlmc_tall_shape(torch_cuda):
     """DLMC's largest shape, 33,288 x 512, at 90% sparsity, bCols 64
     and 4 (Fig. 10's narrow B): exact on the dyadic twin."""
