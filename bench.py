@@ -14,8 +14,10 @@ at {70,80,90,95,98}% x bCols {32,64,128} = 90 SpMMs per step.  With N>1 ranks (t
 problem is row-block sharded (rank r owns rows [r*m/N, (r+1)*m/N), B
 replicated, no collective on the hot path): total work is
 fixed, so scaling is "strong".  The independent problems of a suite run on
---streams S streams (default 4, LPT by flops; forked from and joined into the
-timed stream); the same steps on one stream are reported as "serial".
+--streams S streams (default 16, LPT by flops; forked from and joined into the
+timed stream) on plans autotuned for concurrent throughput (escs_params.autotune
+= 2); the same steps on one stream, on the latency-autotuned plans, are
+reported as "serial".
 
 Timing: W untimed warm-up steps, then K timed steps.  Before each step the L2
 is flushed by writing a 256 MiB buffer (> 126 MB L2), and a device-side sleep
@@ -756,7 +758,7 @@ def run_escs(args):
                               if not args.hot_l2 else "NOT flushed (--hot-l2 diagnostic, not a bench value)"),
                        "plans": (("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates); "
                                   + ("the multi-stream step (value) runs throughput-objective plans (autotune=2: candidates "
-                                     "timed as 4 concurrent copies on 4 streams), serial / per-launch / per-case figures "
+                                     "timed as 8 concurrent launch chains on 8 streams), serial / per-launch / per-case figures "
                                      "the latency-objective plans (autotune=1)" if want_tp else "latency objective (autotune=1)"))
                                  if args.autotune else "parameter table (escs_plan defaults)"),
                        "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}},
@@ -846,7 +848,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--group", type=int, default=0,
                     help="1: each stream's problems in one escs_spmm_group call (grouped launches)")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=16,
                     help="suite: run the independent problems on this many streams (LPT by flops)")
     ap.add_argument("--cases-out", default=None)
     ap.add_argument("--no-tp-plans", dest="tp_plans", action="store_false",

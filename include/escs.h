@@ -201,8 +201,9 @@ typedef struct {
                              still the canonical plan of the chosen (UFi, T).
                              Also enabled by ESCS_AUTOTUNE=1.
                              2: same search, throughput objective: each
-                             candidate is timed as 4 concurrent chains of
-                             its launches on 4 streams (each with its own
+                             candidate is timed as 8 concurrent chains of
+                             its launches on 8 streams (ESCS_TUNE_STREAMS,
+                             2..16; each chain with its own
                              fixup workspace; for callers that overlap
                              independent SpMMs on several streams; prefers
                              plans that leave SMs to the other streams).

@@ -337,10 +337,15 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // matrix and bCols.  Coordinate descent over the item size T (with the auto
 // tile width), then the tile width W, then UFk; every candidate is a complete
 // canonical plan, timed as back-to-back launches (min over 3 batches of 8).
-// Throughput objective (autotune = 2): kTuneStreams copies of a candidate
+// Throughput objective (autotune = 2): ESCS_TUNE_STREAMS copies of a candidate
 // plan (each with its own workspace/counters and C) run concurrently, one per
 // stream, as independent layers of a suite would.
-constexpr int kTuneStreams = 4;
+constexpr int kTuneStreams = 16;  // capacity; ESCS_TUNE_STREAMS (default 8) chains are timed
+int tune_streams() {
+    const char* e = std::getenv("ESCS_TUNE_STREAMS");
+    const int v = e ? std::atoi(e) : 8;
+    return v < 2 ? 2 : v > kTuneStreams ? kTuneStreams : v;
+}
 struct TuneBufs {
     float *vals = nullptr, *B = nullptr, *C = nullptr;
     float* Cx[kTuneStreams] = {};
@@ -440,17 +445,18 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b) {
     }
     const escs::DevPlan* P[kTuneStreams];
     for (int i = 0; i < kTuneStreams; i++) P[i] = &dp[i];
-    for (int i = 0; i < kTuneStreams; i++)
+    const int ns = tune_streams();
+    for (int i = 0; i < ns; i++)
         for (int w = 0; w < 2; w++) escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
     constexpr int kBatch = 8;
     for (int rep = 0; rep < 3; rep++) {
         escs::launch_spin(b.stream, 200000);
         cudaEventRecord(b.e0, b.stream);
-        for (int i = 0; i < kTuneStreams; i++) cudaStreamWaitEvent(b.sx[i], b.e0, 0);
+        for (int i = 0; i < ns; i++) cudaStreamWaitEvent(b.sx[i], b.e0, 0);
         for (int j = 0; j < kBatch; j++)
-            for (int i = 0; i < kTuneStreams; i++)
+            for (int i = 0; i < ns; i++)
                 escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
-        for (int i = 0; i < kTuneStreams; i++) {
+        for (int i = 0; i < ns; i++) {
             cudaEventRecord(b.ex[i], b.sx[i]);
             cudaStreamWaitEvent(b.stream, b.ex[i], 0);
         }
@@ -458,7 +464,7 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b) {
         if (cudaEventSynchronize(b.e1) != cudaSuccess) return 1e30f;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, b.e0, b.e1);
-        best = std::min(best, ms / (kBatch * kTuneStreams));
+        best = std::min(best, ms / (kBatch * ns));
     }
     return best;
 }

@@ -314,7 +314,7 @@ def test_autotuned_plan_parity(torch_cuda):
 
 @pytest.mark.parametrize("shape", [(512, 2048, 0.7, 128), (2048, 512, 0.9, 32)])
 def test_throughput_tuned_plan_parity(torch_cuda, shape):
-    """autotune = 2 (candidates timed as 4 concurrent copies on 4 streams, the
+    """autotune = 2 (candidates timed as 8 concurrent launch chains on 8 streams, the
     plans bench.py's multi-stream step runs): still the canonical plan of its
     (UFi, T), exact on the dyadic twin, and the tuning left the shared
     workspace/counters of the returned plan clean (two calls, same result)."""
@@ -531,22 +531,24 @@ def test_group_graph_capture(torch_cuda):
 
 def test_suite_bench_launch_configuration(torch_cuda):
     """The whole default bench step as bench.py times it: configs[1]+[2]
-    (90 layers), autotuned plans, layers LPT-partitioned over 4 streams forked
+    (90 layers), throughput-autotuned plans (autotune = 2, what the
+    multi-stream step runs), layers LPT-partitioned over 16 streams forked
     from / joined into one stream, PDL chains on each, repeated; every C is
-    bitwise equal to a one-stream run and within the G2 gate of the oracle."""
+    bitwise equal to a one-stream run of the same plans and within the G2
+    gate of the oracle."""
     torch = torch_cuda
     from paper_2506_15174_b200 import escs, shard
     probs = synth.suite()
     dev = []
     for p in probs:
         A = p.A
-        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=1)
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=2)
         dev.append((pl, torch.from_numpy(A.vals).cuda(), torch.from_numpy(p.B).cuda(),
                     torch.full((A.m, p.bcols), float("nan"), device="cuda"),
                     torch.full((A.m, p.bcols), float("nan"), device="cuda")))
     main = torch.cuda.Stream()
-    lanes = [main] + [torch.cuda.Stream() for _ in range(3)]
-    groups = shard.partition_problems([2 * p.A.nnz * p.bcols for p in probs], 4)
+    lanes = [main] + [torch.cuda.Stream() for _ in range(15)]
+    groups = shard.partition_problems([2 * p.A.nnz * p.bcols for p in probs], 16)
     for _ in range(3):
         fork = torch.cuda.Event()
         fork.record(main)
