@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--case", default=None, help="a problem name from bench.py's workloads")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table (default: autotuned, as bench.py)")
+    ap.add_argument("--objective", type=int, default=1,
+                    help="autotune objective: 1 latency (serial/per-case plans), 2 concurrent "
+                         "throughput (the plans bench.py's multi-stream step runs)")
     a = ap.parse_args()
     import torch
     from paper_2506_15174_b200 import escs, synth
@@ -45,7 +48,7 @@ def main():
         r0, r1 = synth.shard_bounds(A.m, world, rank)
         A = synth.row_block(A, r0, r1)
     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
-                           autotune=1 if a.autotune else 0)
+                           autotune=a.objective if a.autotune else 0)
     print(pl.info, flush=True)
     dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
     dC = torch.empty(A.m, B.shape[1], device="cuda")
