@@ -426,6 +426,10 @@ def run_escs(args):
     lanes = [stream] + [torch.cuda.Stream(device) for _ in range(nstreams - 1)]
     groups = shard.partition_problems([d["flops"] for _, d in shard_problems], nstreams)
     owner = {i: g for g, idx in enumerate(groups) for i in idx}
+    # multi-stream issue order: heaviest problems first (LPT list order), so
+    # the long layers start at once and the short ones fill in behind them
+    issue = (sorted(range(len(shard_problems)), key=lambda i: (-shard_problems[i][1]["flops"], i))
+             if args.issue_order == "lpt" else list(range(len(shard_problems))))
 
     # --group: each stream's problems go through ONE escs_spmm_group call (one
     # launch per kernel instance, <= 32 problems each, instead of one per problem)
@@ -466,7 +470,8 @@ def run_escs(args):
             for g, st in zip(grouped, lanes):
                 g(stream=st)
         else:
-            for i, (p, d) in enumerate(shard_problems):
+            for i in issue:
+                p, d = shard_problems[i]
                 st = lanes[owner[i]]
                 if per_launch is not None:
                     per_launch[i][0].record(st)
@@ -848,6 +853,8 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--group", type=int, default=0,
                     help="1: each stream's problems in one escs_spmm_group call (grouped launches)")
+    ap.add_argument("--issue-order", default="lpt", choices=("lpt", "index"),
+                    help="multi-stream step: launch problems heaviest-first (lpt) or in suite order")
     ap.add_argument("--streams", type=int, default=16,
                     help="suite: run the independent problems on this many streams (LPT by flops)")
     ap.add_argument("--cases-out", default=None)
