@@ -150,6 +150,9 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
                  variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0) -> Plan:
+    """escs_plan with explicit escs_params (include/escs.h); 0 = auto for every
+    field.  autotune: 1 = latency objective (one stream), 2 = concurrent
+    throughput objective (independent SpMMs overlapped on several streams)."""
     rowptr, colidx = _csr_args(rowptr, colidx)
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
                 int(nthreads), int(autotune), int(colf), int(tile_order), (ctypes.c_int32 * 2)())
