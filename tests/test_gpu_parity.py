@@ -338,6 +338,28 @@ def test_throughput_tuned_plan_parity(torch_cuda, shape):
     assert np.array_equal(dC.cpu().numpy(), C)
 
 
+@pytest.mark.parametrize("autotune", [1, 2])
+def test_tuned_plans_skewed_and_degenerate(torch_cuda, autotune):
+    """Both tuning objectives on power-law rows (heavy panels: the throughput
+    objective times copies with their own fixup workspace), on a matrix with
+    empty and dense rows, and on nnz = 0: exact on the dyadic twins, and the
+    plan's own counters left clean (a second call gives the same C)."""
+    from paper_2506_15174_b200 import escs
+    cases = [synth.power_law(4096, 4096, 0.99, 7),
+             synth.random_csr(300, 700, 9000, 8, empty_rows=(0, 5, 299), dense_rows=(17, 200)),
+             synth.random_csr(64, 64, 0, 9)]
+    for A0 in cases:
+        A, B = synth.dyadic_twin(A0, 128, 45)
+        C, pl = run_escs(torch_cuda, A, B, autotune=autotune)
+        check_exact(A, B, C)
+        dv = torch_cuda.from_numpy(A.vals).cuda() if A.nnz else torch_cuda.zeros(1, device="cuda")
+        dB = torch_cuda.from_numpy(np.ascontiguousarray(B)).cuda()
+        dC = torch_cuda.empty((A.m, 128), device="cuda")
+        escs.escs_spmm(pl, dv, dB, dC)
+        torch_cuda.cuda.synchronize()
+        assert np.array_equal(dC.cpu().numpy(), C)
+
+
 def test_dlmc_tall_shape(torch_cuda):
     """DLMC's largest shape, 33,288 x 512, at 90% sparsity, bCols 64
     and 4 (Fig. 10's narrow B): exact on the dyadic twin."""
