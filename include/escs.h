@@ -206,7 +206,9 @@ typedef struct {
                              2..16; each chain with its own
                              fixup workspace; for callers that overlap
                              independent SpMMs on several streams; prefers
-                             plans that leave SMs to the other streams).
+                             plans that leave SMs to the other streams;
+                             such plans launch without programmatic
+                             dependent launch).
                              Any other value: ESCS_ERR_ARG.                   */
     int32_t colf;         /* B columns per lane of the vector kernel: the bCols
                              coarsening factor (register tile of B columns,

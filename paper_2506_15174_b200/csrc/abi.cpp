@@ -475,6 +475,11 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     const bool concurrent = q.autotune == 2;
     q.autotune = 0;
     escs_plan_t best = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+    // Throughput plans launch without programmatic dependent launch: with
+    // many streams sharing the SMs, CTAs that start early and wait on the
+    // previous grid hold SM slots the other streams' layers could use (suite
+    // on 16 streams +2%; profiles/r1_notes.md)
+    if (best && concurrent) best->dev.pdl = false;
     if (!best || nnz > 8000000) return best;   // large problems: many waves, heuristic holds
     TuneBufs bufs(m, k, nnz, bCols, concurrent);
     if (!bufs.ok) return best;
@@ -489,6 +494,7 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             clear_error();
             return;
         }
+        if (concurrent) P->dev.pdl = false;
         const float t = timed(P);
         if (t < tb) {
             escs_free(best);
