@@ -383,6 +383,7 @@ def run_escs(args):
     shard_problems = []
     plan_s = 0.0
     plan_info = []
+    plan_info_tp = []
     for idx in mine:
         p = problems[idx]
         t0 = time.perf_counter()
@@ -404,6 +405,7 @@ def run_escs(args):
         plan_s += time.perf_counter() - t0
         info = pl.info
         plan_info.append(info)
+        plan_info_tp.append(pl_tp.info if pl_tp is not None else None)
         d = {"plan": pl, "plan_tp": pl_tp or pl, "A": A,
              "vals": torch.from_numpy(A.vals).to(device) if A.nnz else torch.zeros(1, device=device),
              "B": torch.from_numpy(p.B).to(device),
@@ -766,7 +768,9 @@ def run_escs(args):
                                      "timed as 8 concurrent launch chains on 8 streams), serial / per-launch / per-case figures "
                                      "the latency-objective plans (autotune=1)" if want_tp else "latency objective (autotune=1)"))
                                  if args.autotune else "parameter table (escs_plan defaults)"),
-                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}},
+                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")},
+                       "plan_throughput": ({k: plan_info_tp[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}
+                                           if plan_info_tp[dom] is not None else None)},
             "roofline": {"bound": "hbm", "achieved": step_bytes_per_s, "peak": hbm, "unit": "GB/s",
                          "frac": step_bytes_per_s / hbm, "traffic": traffic,
                          "achieved_how": ("algorithmic bytes of the step / timed step (CUDA events on the "
