@@ -125,23 +125,37 @@ int escs_spmm_group(int32_t n, const escs_plan_t *plans, const float *const *val
                     const float *const *B, float *const *C, void *stream);
 
 /*
- * escs_pack -- the value half of the paper's data transformation ("ANNZ":
- * the nonzeros re-stored in kernel traversal order, §3.3.3; built
- * once and reused across inference calls): packed[s] =
- * vals[slot_src[s]] for s < nnz (Reading R1 slot order).  One kernel launch
- * on `stream`, enqueue-only.
+ * escs_pack -- the value half of the paper's data transformation: the
+ * nonzeros re-stored in kernel traversal order ("ANNZ", §3.3.3),
+ * built once per weight matrix and reused across inference calls
+ * ("TA = dataTransformer(A, UFi, UFk)").  Writes the plan's RECORD
+ * STREAM: one record per gcol j (a (panel, column) pair with a nonzero, in the
+ * canonical gcol order of escs_plan_export), holding the column, the UFi-bit
+ * pattern and the pattern rows' values (Reading R1 slots, stored by row):
+ *   UFi = 1      int32 {col, value}                               2 words
+ *   UFi = 2, 3   int32 {col | mask << 27, w_0 .. w_{h-1}, 0 ..}    4 words
+ *   UFi = 4      int32 {col | mask << 27, w_0, w_1, w_2, w_3, 0, 0, 0}  8 words
+ * (w_r = the value of A(panel*h + r, col), 0.0 for rows outside the pattern;
+ * values are copied bit for bit).  One kernel launch on `stream`,
+ * enqueue-only.
  *   vals    DEVICE float[nnz], CSR order.
- *   packed  DEVICE float[nnz], caller-owned output, must not alias vals.
+ *   packed  DEVICE buffer of escs_plan_stats.packed_words 32-bit words,
+ *           16-byte aligned, caller-owned output; must not alias vals.
  * Returns ESCS_OK, ESCS_ERR_ARG or ESCS_ERR_CUDA.
  */
 int escs_pack(escs_plan_t plan, const float *vals, float *packed, void *stream);
 
 /*
- * escs_spmm_packed -- escs_spmm with values already packed by escs_pack: the
- * kernel reads each chunk's values contiguously instead of through slot_src
- * (one dependent load fewer per chunk at UFi > 1; identical to escs_spmm at
- * UFi = 1, whose slot map is the identity).  Same contract as escs_spmm;
- * the result is bitwise identical to escs_spmm on the unpacked values.
+ * escs_spmm_packed -- C = A x B from the record stream of escs_pack: each
+ * (sub-)warp reads its column's record with one broadcast load (column,
+ * pattern and every row value together), gathers the B row once with 128-bit
+ * loads and reuses it in registers for every row of the pattern (the
+ * enumerated, sparse-coarsened kernel of §3.3 without the slot-map
+ * indirection).  Same contract as escs_spmm (one launch, beta = 0, PDL, graph
+ * capturable); B and C must be 16-byte aligned and the plan must use the
+ * vector kernel (bCols in {4,8,16,32,64,128,256}), else ESCS_ERR_UNSUPPORTED.
+ * For finite B the result is bitwise identical to escs_spmm on the CSR values
+ * (same per-lane FMA order, same combine).
  */
 int escs_spmm_packed(escs_plan_t plan, const float *packed, const float *B, float *C,
                      void *stream);
@@ -171,8 +185,10 @@ int escs_spmm_scatter(escs_plan_t plan, const float *vals, const float *B,
                       float *const *dsts, int32_t n_dst, int64_t row_offset, uint32_t flags,
                       void *stream);
 
-/* Release the plan's host and device memory.  NULL is a no-op.  No call on
- * the plan may be in flight. */
+/* escs_free -- release the plan's host and device memory (the plan owns them,
+ * "TA" of Listing 2, kept until the caller drops it).  NULL is a
+ * no-op.  No call on the plan may be in flight (the caller synchronises the
+ * streams that used it, as with cudaFree). */
 void escs_free(escs_plan_t plan);
 
 /* Code and message of the last failed call on this thread (ESCS_OK and ""
@@ -220,7 +236,13 @@ typedef struct {
                              order, 2 = panels ordered by their longest item
                              (similar work per tile, long tiles first).
                              Searched by the autotuner when 0.               */
-    int32_t reserved[2];  /* must be zero                                        */
+    int32_t packed;       /* 1: the plan will run through escs_pack +
+                             escs_spmm_packed (the record walk): the parameter
+                             table and the autotuner target that walk, and
+                             the tuner also searches UFi in 1..4
+                             unless ufi is given.  0: escs_spmm (CSR values).
+                             Either way any call works on the plan.           */
+    int32_t reserved[1];  /* must be zero                                        */
 } escs_params;
 
 /* escs_plan with explicit parameters; p may be NULL (= all auto). */
@@ -263,6 +285,9 @@ typedef struct {
     int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing */
     int32_t colf;           /* B columns per lane of the launch's lane map (0 scalar map) */
     int32_t tile_order;     /* 1 panel order, 2 by item length (resolved)          */
+    int32_t pdl;            /* 1 if launches carry programmatic dependent launch    */
+    int32_t packed;         /* 1 if planned (and tuned) for escs_spmm_packed         */
+    int64_t packed_words;   /* size of escs_pack's record stream, in 32-bit words   */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);
@@ -275,6 +300,15 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);
  * Its duration is the empirical gather ceiling of this plan.
  */
 int escs_gather_probe(escs_plan_t plan, const float *B, float *sink, void *stream);
+
+/*
+ * escs_gather_probe_packed -- the same for escs_spmm_packed: the record walk
+ * (one broadcast record load per column, the 128-bit B-row gathers) without
+ * the FMAs.  `packed` is the record stream of escs_pack (only the column
+ * words are used).  Same sink contract.
+ */
+int escs_gather_probe_packed(escs_plan_t plan, const float *packed, const float *B, float *sink,
+                             void *stream);
 
 /* Library version string ("escs <ver> sm_100a"). */
 const char *escs_version(void);

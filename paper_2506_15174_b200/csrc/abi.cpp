@@ -67,6 +67,7 @@ void apply_env(escs::Params& p, bool& set_warps) {
             else if (k == "ufk") p.ufk = v;
             else if (k == "colf") p.colf = v;
             else if (k == "order") p.tile_order = v;
+            else if (k == "packed") p.packed = v;
         }
         i = j + 1;
     }
@@ -158,8 +159,19 @@ bool upload(escs_plan_impl* P) {
         items[4 * k + 3] = sb;
     }
     size_t off = 0;
+    // slot of each gcol's first value (escs_pack's record stream, UFi > 1)
+    std::vector<int32_t> vbase;
+    if (h > 1) {
+        vbase.resize(G);
+        for (int64_t g = 0; g < NG; g++) {
+            const int p = __builtin_popcount((unsigned)ph.grp_mask[g]);
+            for (int32_t c = ph.grp_col_ptr[g]; c < ph.grp_col_ptr[g + 1]; c++)
+                vbase[c] = ph.grp_val_ptr[g] + (c - ph.grp_col_ptr[g]) * p;
+        }
+    }
     const size_t o_gpk = add_region<int32_t>(off, G);
     const size_t o_slot = add_region<int32_t>(off, nnz);
+    const size_t o_vb = add_region<int32_t>(off, vbase.size());
     const size_t o_items = add_region<int32_t>(off, 4 * NS);
     const size_t o_aux = add_region<int32_t>(off, NS);
     const size_t o_tiles = add_region<int32_t>(off, ph.tile_heavy.size());
@@ -186,6 +198,7 @@ bool upload(escs_plan_impl* P) {
     };
     if (!put(o_gpk, gpk.data(), G * 4)) return false;
     if (!put(o_slot, ph.slot_src.data(), nnz * 4)) return false;
+    if (!put(o_vb, vbase.data(), vbase.size() * 4)) return false;
     if (!put(o_items, items.data(), items.size() * 4)) return false;
     if (!put(o_aux, ph.slot_aux.data(), NS * 4)) return false;
     if (!put(o_tiles, ph.tile_heavy.data(), ph.tile_heavy.size() * 4)) return false;
@@ -193,6 +206,7 @@ bool upload(escs_plan_impl* P) {
     if (ph.n_heavy) CUDA_TRY(cudaMemset(b + o_cnt, 0, ph.n_heavy * 4));
     dp.gpk = reinterpret_cast<const int32_t*>(b + o_gpk);
     dp.slot = reinterpret_cast<const int32_t*>(b + o_slot);
+    dp.vbase = h > 1 ? reinterpret_cast<const int32_t*>(b + o_vb) : nullptr;
     dp.items = reinterpret_cast<const int32_t*>(b + o_items);
     dp.item_aux = reinterpret_cast<const int32_t*>(b + o_aux);
     dp.tile_heavy = reinterpret_cast<const int32_t*>(b + o_tiles);
@@ -220,11 +234,14 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         return nullptr;
     }
     if (ep) {
-        for (int i = 0; i < 2; i++)
-            if (ep->reserved[i] != 0) {
-                fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
-                return nullptr;
-            }
+        if (ep->reserved[0] != 0) {
+            fail(ESCS_ERR_ARG, "escs_params.reserved must be zero");
+            return nullptr;
+        }
+        if (ep->packed < 0 || ep->packed > 1) {
+            fail(ESCS_ERR_ARG, "escs_params.packed must be 0 or 1");
+            return nullptr;
+        }
     }
     std::string v = escs::validate_csr(m, k, nnz, rowptr, colidx);
     if (!v.empty()) {
@@ -240,11 +257,14 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
             return nullptr;
         }
     }
-    escs::Params p = escs::choose_params(m, k, nnz, bCols, host_only ? 148 : sm_count_of_current_device());
+    const bool want_packed = ep && ep->packed;
+    escs::Params p = escs::choose_params(m, k, nnz, bCols, host_only ? 148 : sm_count_of_current_device(),
+                                         ep ? ep->ufi : 0, want_packed);
     bool set_warps = false;
     apply_env(p, set_warps);
     if (ep) {
         if (ep->ufi) p.h = ep->ufi;
+        if (ep->packed) p.packed = 1;
         if (ep->T) p.T = ep->T;
         if (ep->cta_warps) { p.cta_warps = ep->cta_warps; set_warps = true; }
         if (ep->variant) p.variant = ep->variant;
@@ -267,17 +287,25 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         fail(ESCS_ERR_UNSUPPORTED, "device plans need k < 2^27 (packed column words)");
         return nullptr;
     }
-    if (p.variant != 1) p.colf = 0;
-    else if (p.colf == 0) p.colf = escs::default_colf(bCols);
+    if (p.variant != 1) {
+        p.colf = 0;
+        p.packed = 0;   // the record walk needs the vector lane map: a CSR-walk plan
+    } else if (p.colf == 0) {
+        p.colf = escs::default_colf(bCols);
+    }
+    // the record walk has every coarsening factor at every UFi; the CSR walk
+    // has the alternative factors at UFi = 1 only (tools/gen_kernels.py)
+    if (!p.packed && p.h > 1 && p.variant == 1) p.colf = escs::default_colf(bCols);
     // automatic UFk: fall back to the largest UFk the chosen lane map has
     // (wide per-lane tiles carry fewer rows in flight: UFk x colf <= 64)
     if (!host_only && !(ep && ep->ufk) && !std::getenv("ESCS_PARAMS"))
-        while (p.ufk > 1 && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf)) p.ufk /= 2;
-    if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf)) {
+        while (p.ufk > 1 && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf, p.packed))
+            p.ufk /= 2;
+    if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf, p.packed)) {
         fail(ESCS_ERR_UNSUPPORTED, "no kernel for ufi=" + std::to_string(p.h) + " bCols=" +
                                        std::to_string(bCols) + " variant=" +
                                        std::to_string(p.variant) + " ufk=" + std::to_string(p.ufk) +
-                                       " colf=" + std::to_string(p.colf));
+                                       " colf=" + std::to_string(p.colf) + (p.packed ? " (packed)" : ""));
         return nullptr;
     }
     escs_plan_impl* P = new (std::nothrow) escs_plan_impl();
@@ -309,6 +337,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     dp.m = (int)m; dp.k = (int)k; dp.nnz = (int)nnz; dp.bcols = bCols; dp.h = p.h;
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
     dp.ufk = p.ufk; dp.colf = p.colf; dp.any_sync = P->host.any_sync;
+    dp.G = P->host.header[9];
     {
         const char* e = std::getenv("ESCS_PDL");
         dp.pdl = !(e && e[0] == '0');
@@ -348,31 +377,75 @@ int tune_streams() {
 }
 struct TuneBufs {
     float *vals = nullptr, *B = nullptr, *C = nullptr;
+    float* packed = nullptr;          // record stream of the candidate (packed objective)
+    size_t packed_cap = 0;            // words
     float* Cx[kTuneStreams] = {};
     cudaStream_t stream = nullptr;
     cudaStream_t sx[kTuneStreams] = {};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaEvent_t ex[kTuneStreams] = {};
+    int ns = 0;                       // concurrent chains timed (0: latency objective)
     // per-stream heavy-panel workspace + counters for the concurrent copies
     // (zeroed once; every launch leaves its counters at zero again)
     float* wsx[kTuneStreams] = {};
     int32_t* cntx[kTuneStreams] = {};
     size_t ws_cap = 0, cnt_cap = 0;
-    bool scratch(size_t ws_elems, size_t n_cnt) {
-        if (ws_elems <= ws_cap && n_cnt <= cnt_cap) return true;
-        cudaDeviceSynchronize();
-        ws_cap = std::max(ws_cap, ws_elems);
-        cnt_cap = std::max(cnt_cap, n_cnt);
+    void free_scratch() {
         for (int i = 0; i < kTuneStreams; i++) {
             if (wsx[i]) cudaFree(wsx[i]);
             if (cntx[i]) cudaFree(cntx[i]);
-            wsx[i] = nullptr; cntx[i] = nullptr;
-            if (cudaMalloc(&wsx[i], ws_cap * 4) != cudaSuccess ||
-                cudaMalloc(&cntx[i], cnt_cap * 4) != cudaSuccess ||
-                cudaMemset(cntx[i], 0, cnt_cap * 4) != cudaSuccess)
-                return false;
+            wsx[i] = nullptr;
+            cntx[i] = nullptr;
         }
-        return cudaDeviceSynchronize() == cudaSuccess;
+        ws_cap = cnt_cap = 0;
+    }
+    // Grow the per-stream workspaces.  The capacities are raised only after
+    // every allocation succeeded; on failure everything is released (caps 0),
+    // so a later call cannot mistake a partial set for a usable one.
+    bool scratch(size_t ws_elems, size_t n_cnt) {
+        if (ws_elems <= ws_cap && n_cnt <= cnt_cap) return true;
+        cudaDeviceSynchronize();
+        const size_t wc = std::max(ws_cap, ws_elems), cc = std::max(cnt_cap, n_cnt);
+        free_scratch();
+        for (int i = 0; i < ns; i++) {
+            if (cudaMalloc(&wsx[i], std::max<size_t>(wc, 1) * 4) != cudaSuccess ||
+                cudaMalloc(&cntx[i], std::max<size_t>(cc, 1) * 4) != cudaSuccess ||
+                cudaMemset(cntx[i], 0, std::max<size_t>(cc, 1) * 4) != cudaSuccess) {
+                cudaGetLastError();
+                free_scratch();
+                return false;
+            }
+        }
+        if (cudaDeviceSynchronize() != cudaSuccess) {
+            cudaGetLastError();
+            free_scratch();
+            return false;
+        }
+        ws_cap = wc;
+        cnt_cap = cc;
+        return true;
+    }
+    // the candidate's record stream (packed objective): escs_pack of the
+    // tuning values into a buffer grown on demand
+    bool pack_for(const escs::DevPlan& dp) {
+        const size_t w = (size_t)escs::packed_words(dp);
+        if (w > packed_cap) {
+            cudaDeviceSynchronize();
+            if (packed) cudaFree(packed);
+            packed = nullptr;
+            packed_cap = 0;
+            if (cudaMalloc(&packed, std::max<size_t>(w, 4) * 4) != cudaSuccess) {
+                cudaGetLastError();
+                packed = nullptr;
+                return false;
+            }
+            packed_cap = w;
+        }
+        if (escs::launch_pack(dp, vals, packed, stream) != 0) {
+            cudaGetLastError();
+            return false;
+        }
+        return true;
     }
     bool ok = false;
     TuneBufs(int64_t m, int64_t k, int64_t nnz, int32_t n, bool concurrent) {
@@ -383,15 +456,18 @@ struct TuneBufs {
              cudaMemset(B, 0, (size_t)k * n * 4) == cudaSuccess &&
              cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) == cudaSuccess &&
              cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
-        for (int i = 0; ok && concurrent && i < kTuneStreams; i++)
+        ns = concurrent ? tune_streams() : 0;
+        for (int i = 0; ok && i < ns; i++)
             ok = cudaMalloc(&Cx[i], (size_t)m * n * 4) == cudaSuccess &&
                  cudaStreamCreateWithFlags(&sx[i], cudaStreamNonBlocking) == cudaSuccess &&
                  cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) cudaGetLastError();
     }
     ~TuneBufs() {
         if (vals) cudaFree(vals);
         if (B) cudaFree(B);
         if (C) cudaFree(C);
+        if (packed) cudaFree(packed);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (stream) cudaStreamDestroy(stream);
@@ -399,26 +475,39 @@ struct TuneBufs {
             if (Cx[i]) cudaFree(Cx[i]);
             if (sx[i]) cudaStreamDestroy(sx[i]);
             if (ex[i]) cudaEventDestroy(ex[i]);
-            if (wsx[i]) cudaFree(wsx[i]);
-            if (cntx[i]) cudaFree(cntx[i]);
         }
+        free_scratch();
         cudaGetLastError();
     }
 };
 
-float time_plan(escs_plan_t P, TuneBufs& b) {
-    float best = 1e30f;
+constexpr float kFailed = 1e30f;
+
+// Latency objective: batches of 16 back-to-back launches queued behind a
+// ~100 us busy-wait (the host enqueues the batch while the GPU spins): GPU
+// time only; min over 3 batches.  A candidate whose launch fails is rejected
+// (time kFailed, CUDA error cleared) -- it must never win by timing no work.
+float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
+    float best = kFailed;
     const bool vec = aligned16(b.B) && aligned16(b.C);
-    for (int w = 0; w < 2; w++) escs::launch_spmm(P->dev, b.vals, b.B, b.C, b.stream, vec);
-    // batches of 16 back-to-back launches queued behind a ~100 us busy-wait
-    // (the host enqueues the batch while the GPU spins): GPU time only
+    if (packed && !b.pack_for(P->dev)) return kFailed;
+    const float* v = packed ? b.packed : b.vals;
+    for (int w = 0; w < 2; w++)
+        if (escs::launch_spmm(P->dev, v, b.B, b.C, b.stream, vec, packed) != 0) {
+            cudaGetLastError();
+            return kFailed;
+        }
     constexpr int kBatch = 16;
     for (int rep = 0; rep < 3; rep++) {
         escs::launch_spin(b.stream, 200000);
         cudaEventRecord(b.e0, b.stream);
-        for (int i = 0; i < kBatch; i++) escs::launch_spmm(P->dev, b.vals, b.B, b.C, b.stream, vec);
+        bool ok = true;
+        for (int i = 0; i < kBatch; i++) ok = ok && escs::launch_spmm(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
         cudaEventRecord(b.e1, b.stream);
-        if (cudaEventSynchronize(b.e1) != cudaSuccess) return 1e30f;
+        if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            return kFailed;
+        }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, b.e0, b.e1);
         best = std::min(best, ms / kBatch);
@@ -429,39 +518,48 @@ float time_plan(escs_plan_t P, TuneBufs& b) {
 // Throughput objective: the copies run one per stream, each stream a chain of
 // kBatch launches, all released together after the busy-wait; time per
 // launch = span / (kBatch * copies).
-float time_plans_concurrent(escs_plan_t P0, TuneBufs& b) {
-    float best = 1e30f;
+float time_plans_concurrent(escs_plan_t P0, TuneBufs& b, bool packed) {
+    float best = kFailed;
     const bool vec = aligned16(b.B) && aligned16(b.C);
     // the copies share the read-only plan arrays; each has its own workspace
     // and counters (one plan must not run on two streams at once)
-    escs::DevPlan dp[kTuneStreams];
     const auto& ph = P0->host;
     if (!b.scratch((size_t)ph.n_heavy_tiles * P0->dev.h * P0->dev.bcols, (size_t)ph.n_heavy))
-        return 1e30f;
-    for (int i = 0; i < kTuneStreams; i++) {
+        return kFailed;
+    if (packed && !b.pack_for(P0->dev)) return kFailed;
+    const float* v = packed ? b.packed : b.vals;
+    const int ns = b.ns;
+    escs::DevPlan dp[kTuneStreams];
+    for (int i = 0; i < ns; i++) {
         dp[i] = P0->dev;
         dp[i].ws = b.wsx[i];
         dp[i].counters = b.cntx[i];
     }
-    const escs::DevPlan* P[kTuneStreams];
-    for (int i = 0; i < kTuneStreams; i++) P[i] = &dp[i];
-    const int ns = tune_streams();
+    if (cudaStreamSynchronize(b.stream) != cudaSuccess) return kFailed;   // pack done
     for (int i = 0; i < ns; i++)
-        for (int w = 0; w < 2; w++) escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
+        for (int w = 0; w < 2; w++)
+            if (escs::launch_spmm(dp[i], v, b.B, b.Cx[i], b.sx[i], vec, packed) != 0) {
+                cudaGetLastError();
+                return kFailed;
+            }
     constexpr int kBatch = 8;
     for (int rep = 0; rep < 3; rep++) {
         escs::launch_spin(b.stream, 200000);
         cudaEventRecord(b.e0, b.stream);
         for (int i = 0; i < ns; i++) cudaStreamWaitEvent(b.sx[i], b.e0, 0);
+        bool ok = true;
         for (int j = 0; j < kBatch; j++)
             for (int i = 0; i < ns; i++)
-                escs::launch_spmm(*P[i], b.vals, b.B, b.Cx[i], b.sx[i], vec);
+                ok = ok && escs::launch_spmm(dp[i], v, b.B, b.Cx[i], b.sx[i], vec, packed) == 0;
         for (int i = 0; i < ns; i++) {
             cudaEventRecord(b.ex[i], b.sx[i]);
             cudaStreamWaitEvent(b.stream, b.ex[i], 0);
         }
         cudaEventRecord(b.e1, b.stream);
-        if (cudaEventSynchronize(b.e1) != cudaSuccess) return 1e30f;
+        if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            return kFailed;
+        }
         float ms = 0.f;
         cudaEventElapsedTime(&ms, b.e0, b.e1);
         best = std::min(best, ms / (kBatch * ns));
@@ -469,10 +567,19 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b) {
     return best;
 }
 
+// The paper's scheduler & tuner (§3.5) is profiling-based: here the
+// profiling runs at plan time, on the device the plan is bound to, for this
+// matrix and bCols.  Coordinate descent: UFi first (the tuner's
+// first parameter; for plans of the record walk, where the enumeration's B-row
+// reuse pays), then the item size T (with the auto tile width), the tile width
+// W, UFk, the bCols coarsening factor and the tile order; every candidate is a
+// complete canonical plan, timed by the chosen objective on the walk it will
+// run (packed: escs_pack then escs_spmm_packed launches).
 escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                                 const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     escs_params q = ep ? *ep : escs_params{};
     const bool concurrent = q.autotune == 2;
+    const bool packed = q.packed != 0;
     q.autotune = 0;
     escs_plan_t best = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
     // Throughput plans launch without programmatic dependent launch: with
@@ -481,11 +588,11 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     // on 16 streams +2%; profiles/r1_notes.md)
     if (best && concurrent) best->dev.pdl = false;
     if (!best || nnz > 8000000) return best;   // large problems: many waves, heuristic holds
+    if (packed && best->dev.variant != 1) return best;   // the record walk needs the vector map
     TuneBufs bufs(m, k, nnz, bCols, concurrent);
     if (!bufs.ok) return best;
-    // a candidate's time under the chosen objective
     auto timed = [&](escs_plan_t P) -> float {
-        return concurrent ? time_plans_concurrent(P, bufs) : time_plan(P, bufs);
+        return concurrent ? time_plans_concurrent(P, bufs, packed) : time_plan(P, bufs, packed);
     };
     float tb = timed(best);
     auto consider = [&](escs_params c) {
@@ -504,7 +611,30 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             escs_free(P);
         }
     };
+    // stage 0 (record walk): UFi jointly with the item size and the tile
+    // width -- the paper's tuner searches UFi first; on B200 the
+    // best UFi > 1 plans need short items in narrow tiles (many warps per
+    // panel, combined through the workspace), which a descent that fixes T
+    // before W never reaches (profiles/r2_notes.md).  Items per panel
+    // {1, 3, 8, 24} x tile width {auto, 4, 16}, from the expected panel stream
+    // k(1 - s^h) of a uniformly pruned matrix.
+    if (packed && !(ep && ep->ufi)) {
+        const double dens = (double)nnz / ((double)m * (double)k);
+        for (int h : {1, 2, 3, 4}) {
+            const double sp = (double)k * (1.0 - std::pow(1.0 - dens, h));
+            const int pw[6][2] = {{1, 0}, {3, 0}, {8, 4}, {8, 16}, {24, 4}, {24, 16}};
+            for (const auto& x : pw) {
+                if (ep && ep->T && x[0] != 1) continue;
+                escs_params c = q;
+                c.ufi = h;
+                if (!(ep && ep->T)) c.T = std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / x[0]));
+                if (!(ep && ep->cta_warps)) c.cta_warps = x[1];
+                consider(c);
+            }
+        }
+    }
     const int h = best->params.h;
+    const int F_best = best->dev.variant == 1 ? best->params.colf : 0;
     // stage 1: item size T (tile width follows automatically)
     if (!(ep && ep->T)) {
         const double nP = (double)best->host.header[7];
@@ -521,6 +651,8 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             escs_params c = q;
             c.ufi = h;
             c.T = T;
+            c.colf = F_best;
+            c.ufk = best->params.ufk;
             consider(c);
         }
     }
@@ -537,36 +669,40 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             c.ufi = h;
             c.T = T;
             c.cta_warps = W;
+            c.colf = F_best;
+            c.ufk = best->params.ufk;
             consider(c);
         }
     }
     // stage 3: rows in flight
     if (!(ep && ep->ufk)) {
         const int U0 = best->params.ufk;
-        for (int U : {4, 8}) {
-            if (U == U0 || bCols < 32) continue;
+        for (int U : {2, 4, 8}) {
+            if (U == U0 || bCols < 32 || (U == 2 && !packed)) continue;
             escs_params c = q;
             c.ufi = h;
             c.T = best->params.T;
             c.cta_warps = best->params.cta_warps;
+            c.colf = F_best;
             c.ufk = U;
             consider(c);
         }
     }
     // stage 4: B columns per lane (bCols coarsening of the vector lane map;
-    // wider per-lane tiles trade shuffles per gathered row for fewer lanes)
-    if (!(ep && ep->colf) && best->params.h == 1 && best->dev.variant == 1) {
+    // wider per-lane tiles trade shuffles per gathered row for fewer lanes);
+    // the CSR walk has the alternative factors at UFi = 1 only
+    if (!(ep && ep->colf) && (best->params.h == 1 || packed) && best->dev.variant == 1) {
         const int F0 = best->params.colf;
         for (int F : {4, 8, 16}) {
             if (F == F0) continue;
             for (int U : {best->params.ufk, 4, 2}) {
                 escs_params c = q;
-                c.ufi = 1;
+                c.ufi = best->params.h;
                 c.T = best->params.T;
                 c.cta_warps = best->params.cta_warps;
                 c.ufk = U;
                 c.colf = F;
-                if (!escs::kernel_supported(1, bCols, 1, U, F)) continue;
+                if (!escs::kernel_supported(c.ufi, bCols, 1, U, F, packed)) continue;
                 consider(c);
                 break;
             }
@@ -627,6 +763,11 @@ static int spmm_common(escs_plan_t plan, const float* vals, const float* B, floa
                                       " differs from the plan's device " +
                                       std::to_string(plan->device));
     const bool vec_ok = aligned16(B) && aligned16(C);
+    if (packed && !(vec_ok && plan->dev.variant == 1))
+        return fail(ESCS_ERR_UNSUPPORTED, "escs_spmm_packed needs 16-byte aligned B and C and a "
+                                          "vector-kernel plan (bCols in {4,8,16,32,64,128,256})");
+    if (packed && vals && !aligned16(vals))
+        return fail(ESCS_ERR_ARG, "the packed record stream must be 16-byte aligned");
     int e = escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok, packed);
     if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
@@ -659,7 +800,7 @@ int escs_spmm_group(int32_t n, const escs_plan_t* plans, const float* const* val
                 return fail(ESCS_ERR_ARG, "a plan appears twice in one group (shared workspace)" + at);
         dps[i] = &P->dev;
     }
-    int e = escs::launch_group(n, dps.data(), vals, B, C, stream, false);
+    int e = escs::launch_group(n, dps.data(), vals, B, C, stream);
     if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
     return ESCS_OK;
@@ -701,10 +842,11 @@ int escs_spmm_packed(escs_plan_t plan, const float* packed, const float* B, floa
 int escs_pack(escs_plan_t plan, const float* vals, float* packed, void* stream) {
     clear_error();
     if (!plan || plan->host_only) return fail(ESCS_ERR_ARG, "plan is NULL or host-only");
-    if (plan->host.header[3] > 0 && (!vals || !packed))
+    if (plan->host.header[9] > 0 && (!vals || !packed))
         return fail(ESCS_ERR_ARG, "vals and packed must be non-NULL device pointers");
-    if (vals == packed && plan->host.header[3] > 0)
+    if (vals == packed && plan->host.header[9] > 0)
         return fail(ESCS_ERR_ARG, "packed must not alias vals");
+    if (packed && !aligned16(packed)) return fail(ESCS_ERR_ARG, "packed must be 16-byte aligned");
     int e = escs::launch_pack(plan->dev, vals, packed, stream);
     if (e) return fail(ESCS_ERR_CUDA, std::string("pack launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
@@ -716,6 +858,19 @@ int escs_gather_probe(escs_plan_t plan, const float* B, float* sink, void* strea
     if (!plan || plan->host_only || !B || !sink) return fail(ESCS_ERR_ARG, "bad probe arguments");
     const bool vec_ok = aligned16(B);
     int e = escs::launch_probe(plan->dev, B, sink, stream, vec_ok);
+    if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") +
+                                                 cudaGetErrorString((cudaError_t)e));
+    return ESCS_OK;
+}
+
+int escs_gather_probe_packed(escs_plan_t plan, const float* packed, const float* B, float* sink,
+                             void* stream) {
+    clear_error();
+    if (!plan || plan->host_only || !B || !sink || (!packed && plan->host.header[9] > 0))
+        return fail(ESCS_ERR_ARG, "bad probe arguments");
+    static const float dummy[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* rec = packed ? packed : dummy;   // G = 0: no record is read
+    int e = escs::launch_probe(plan->dev, B, sink, stream, aligned16(B), rec);
     if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") +
                                                  cudaGetErrorString((cudaError_t)e));
     return ESCS_OK;
@@ -772,10 +927,19 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->device_bytes = (int64_t)plan->dbytes;
     o->workspace_bytes = (int64_t)plan->ws_bytes;
     o->plan_seconds = h.plan_seconds;
-    o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false);
+    o->packed = plan->params.packed;
+    o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false,
+                                                               o->packed != 0);
     o->autotuned = plan->autotuned ? 1 : 0;
     o->colf = plan->dev.variant == 1 ? plan->params.colf : 0;
     o->tile_order = plan->params.tile_order;
+    o->pdl = plan->dev.pdl ? 1 : 0;
+    {
+        escs::DevPlan d = plan->dev;   // host-only plans: the same formula from the header
+        d.h = h.header[5];
+        d.G = h.header[9];
+        o->packed_words = escs::packed_words(d);
+    }
     return ESCS_OK;
 }
 

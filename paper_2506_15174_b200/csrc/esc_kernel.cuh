@@ -36,8 +36,13 @@ constexpr int kColBits = 27;                       // packed gcol: col | mask <<
 constexpr int kColMask = (1 << kColBits) - 1;
 constexpr int kMaxScatter = 8;
 #ifndef ESC_MINB
-#define ESC_MINB 1   // min resident 512-thread blocks per SM in __launch_bounds__
-#endif                     // escs_spmm_scatter destinations
+#define ESC_MINB 1   // min resident 512-thread blocks per SM in __launch_bounds__ (0: none)
+#endif
+#if ESC_MINB > 0
+#define ESC_CSR_BOUNDS __launch_bounds__(512, ESC_MINB)
+#else
+#define ESC_CSR_BOUNDS __launch_bounds__(512)
+#endif
 
 struct KParams {
     const int* __restrict__ gpk;       // packed gcols: column | pattern << 27
@@ -48,8 +53,7 @@ struct KParams {
     const int4* __restrict__ heavy;    // panel, ws_base, ntiles, 0
     float* ws;
     int* counters;                     // heavy-panel arrival counters
-    int packed;                        // vals already in slot order (escs_pack)
-    const float* __restrict__ vals;
+    const float* __restrict__ vals;    // CSR values, or the packed record stream (kRec)
     const float* __restrict__ B;
     float* __restrict__ C;
     int m, n;
@@ -132,8 +136,11 @@ struct VecMap {
         return F <= 4 ? lj * F + f : (((f >> 2) * L + lj) << 2) + (f & 3);
     }
     __device__ static __forceinline__ void load(float (&b)[F], const float* row, int, int lj) {
+        load_pol(b, row, lj, policy_last());
+    }
+    __device__ static __forceinline__ void load_pol(float (&b)[F], const float* row, int lj,
+                                                    unsigned long long pol) {
         const float* q = row + (F <= 4 ? lj * F : 4 * lj);
-        const unsigned long long pol = policy_last();
         if constexpr (F == 1) {
             asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;"
                          : "=f"(b[0]) : "l"(q), "l"(pol));
@@ -340,7 +347,7 @@ __device__ __forceinline__ void walk1(const PP& p, int beg, int end, int sbase,
 // flight, so no dependent global round trip sits between two chunks' FMAs.
 // slot_addr: this lane's value positions for a chunk (exclusive warp scan of
 // the popcounts, Reading R1 order) -- the slot-map loads for CSR-ordered
-// values, or the positions themselves when the values are pre-packed.
+// values.
 template <int H, class PP>
 __device__ __forceinline__ int slot_addr(const PP& p, int pk, int sbase, int lane,
                                          int (&sl)[H]) {
@@ -356,7 +363,7 @@ __device__ __forceinline__ int slot_addr(const PP& p, int pk, int sbase, int lan
 #pragma unroll
     for (int r = 0; r < H; r++) {
         const int pos = sbase + excl + __popc(mask & ((1u << r) - 1u));
-        sl[r] = ((mask >> r) & 1u) ? (p.packed ? pos : ld_stream(p.slot + pos)) : -1;
+        sl[r] = ((mask >> r) & 1u) ? ld_stream(p.slot + pos) : -1;
     }
     return sbase + total;
 }
@@ -442,6 +449,98 @@ __device__ __forceinline__ void walk(const PP& p, Stage<H>& st, int beg, int end
     }
 }
 
+// ---------------------------------------------------------------- records
+// Kernel modes: the CSR-value walks above (kCsr, and their gather probe), or
+// the record walk below over the packed stream written by escs_pack (kRec,
+// and its probe).
+enum Mode { kCsr = 0, kProbe = 1, kRec = 2, kRecProbe = 3 };
+
+// The packed record stream (escs_pack; the paper's data transformation that
+// stores the nonzeros in kernel traversal order, "ANNZ", §3.3.3 P:455-493,
+// built once per weight matrix and reused across calls): one record
+// per gcol j, in canonical gcol order, values stored BY PATTERN ROW (0.0 for
+// the rows outside the pattern; they are never multiplied, the FMAs are
+// predicated on the pattern bits):
+//   UFi = 1      int2 {col, value}                              ( 8 bytes)
+//   UFi = 2, 3   int4 {col | mask << 27, w_0, .., w_{h-1}, 0..}  (16 bytes)
+//   UFi = 4      2 x int4 {col | mask << 27, w_0, w_1, w_2}, {w_3, 0, 0, 0}
+// A (sub-)warp reads its column's record with ONE broadcast load (all lanes
+// of the sub-warp the same address: one L1 wavefront), so the column index,
+// the pattern and every value arrive together: no shuffles, no slot map, no
+// shared-memory staging.  The B row is then gathered with 128-bit loads and
+// reused in registers for every row of the pattern (§3.3.2).
+template <int H>
+struct RecFmt {
+    static constexpr int W = H == 1 ? 2 : (H <= 3 ? 4 : 8);   // int words per record
+};
+
+template <int RW>
+__device__ __forceinline__ void ld_rec(int (&r)[RW], const int* q) {
+    if constexpr (RW == 2) {
+        asm volatile("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "l"(q));
+    } else {
+        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(q));
+        if constexpr (RW == 8) asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(r[4]) : "l"(q + 4));
+    }
+}
+
+// One batch of U records per sub-warp (U*S records per warp): record loads,
+// then the U gathered B rows, then the pattern rows' FMAs.  TAIL: the batch
+// crosses the item end; a past-the-end slot re-reads the item's last record
+// (a valid address) and multiplies nothing (pattern cleared, or the UFi = 1
+// FMA predicated off).  The records are read with plain L1-allocating loads:
+// a 128-byte line holds the next 4-16 records of the (sub-)warp.
+template <int H, class Map, int U, bool TAIL, bool PROBE, class PP>
+__device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, int end, int sub,
+                                          int lj, float (&acc)[H][Map::F], unsigned long long pol_b) {
+    constexpr int F = Map::F, S = Map::S, RW = RecFmt<H>::W, N = Map::L * Map::F;
+    int r[U][RW];
+    float b[U][F];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int idx = i + u * S + sub;
+        ld_rec<RW>(r[u], rec + (size_t)(TAIL ? min(idx, end - 1) : idx) * RW);
+        if (TAIL && H > 1 && idx >= end) r[u][0] &= kColMask;   // no pattern rows
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const int col = H == 1 ? r[u][0] : (r[u][0] & kColMask);
+        Map::load_pol(b[u], p.B + (size_t)col * N, lj, pol_b);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        if constexpr (PROBE) {
+#pragma unroll
+            for (int f = 0; f < F; f++) acc[0][f] += b[u][f];
+        } else if constexpr (H == 1) {
+            if (!TAIL || i + u * S + sub < end) fma_row<F>(acc[0], __int_as_float(r[u][1]), b[u]);
+        } else {
+            const unsigned mk = (unsigned)r[u][0] >> kColBits;
+#pragma unroll
+            for (int row = 0; row < H; row++)
+                if ((mk >> row) & 1u) fma_row<F>(acc[row], __int_as_float(r[u][1 + row]), b[u]);
+        }
+    }
+}
+
+// Walk one item's records [beg, end) (record j = canonical gcol j).
+template <int H, class Map, int U, bool PROBE, class PP>
+__device__ __forceinline__ void walk_rec(const PP& p, int beg, int end, float (&acc)[H][Map::F],
+                                         int lane) {
+    static_assert(Map::kVec, "the record walk uses the vector lane maps");
+    constexpr int US = U * Map::S;
+    static_assert(32 % US == 0, "UFK * sub-warps must divide 32");
+    const int sub = lane / Map::L, lj = lane % Map::L;
+    const int* rec = reinterpret_cast<const int*>(p.vals);
+    const unsigned long long pol_b = policy_last();
+    grid_dep_wait();   // records and B are caller data
+    int i = beg;
+#pragma unroll 1
+    for (; i + US <= end; i += US) rec_batch<H, Map, U, false, PROBE, PP>(p, rec, i, end, sub, lj, acc, pol_b);
+    if (i < end) rec_batch<H, Map, U, true, PROBE, PP>(p, rec, i, end, sub, lj, acc, pol_b);
+}
+
 // Row r of a panel tile is written by sub-warp r % S (after the sub-warp
 // reduction every sub-warp holds the totals).
 template <int H, class Map, class PP>
@@ -463,10 +562,129 @@ __device__ __forceinline__ void store_rows(const PP& p, int panel, const float (
     }
 }
 
-template <int H, class Map>
+// Per-warp shared memory: the CSR walk's staging area (UFi > 1) and the
+// combine partial (H x bCols floats) share it; the record walk needs only the
+// partial.
+template <int H, class Map, int MODE = kCsr>
 __host__ __device__ constexpr int warp_smem_floats() {
-    return (int)(sizeof(Stage<H>) / 4) > H * Map::L * Map::F ? (int)(sizeof(Stage<H>) / 4)
-                                                               : H * Map::L * Map::F;
+    return (MODE < kRec && H > 1 && (int)(sizeof(Stage<H>) / 4) > H * Map::L * Map::F)
+               ? (int)(sizeof(Stage<H>) / 4) : H * Map::L * Map::F;
+}
+
+// Store one value group of an output row: C and the fused all-gather
+// destinations (escs_spmm_scatter), V = 4 (float4) or 1 consecutive floats.
+template <int V, class PP>
+__device__ __forceinline__ void store_out(const PP& p, int row, int c, const float (&v)[V]) {
+    if (p.C) {
+        if constexpr (V == 4) *reinterpret_cast<float4*>(p.C + (size_t)row * p.n + c) = make_float4(v[0], v[1], v[2], v[3]);
+        else p.C[(size_t)row * p.n + c] = v[0];
+    }
+    if constexpr (PP::kScatter) {
+        for (int d = 0; d < p.n_extra; d++) {
+            float* q = p.extra[d] + (size_t)(p.row_off + row) * p.n + c;
+            if constexpr (V == 4) {
+                if (p.mc)
+                    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                                 :: "l"(q), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]) : "memory");
+                else *reinterpret_cast<float4*>(q) = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+                if (p.mc) asm volatile("multimem.st.weak.global.f32 [%0], %1;" :: "l"(q), "f"(v[0]) : "memory");
+                else q[0] = v[0];
+            }
+        }
+    }
+}
+
+// Heavy panel (more items than the tile's warps; power-law rows, long rows
+// split for parallelism): its tiles combine through the global workspace.
+// Every warp of the tile takes part (the slots of the H x bCols output are
+// spread over the CTA's threads): the tile's item partials are summed from
+// shared memory in item order into the tile's workspace slice; the
+// last-arriving tile (counter) sums the tiles' slices in tile order and
+// writes C.  The order of every sum is fixed -- deterministic -- and each
+// thread keeps all the tiles' loads of its slots in flight (one round trip
+// for the last tile instead of one per tile).  The barriers are named
+// (barrier 1, the tile's W warps only) so that the idle warps of a grouped
+// launch's wider CTA need not take part.
+template <int H, class Map, class PP>
+__device__ __forceinline__ void heavy_combine(const PP& p, const float* smem, int tile, int w, int lane,
+                                           int W, int cnt, int lead, int WS) {
+    constexpr int NR = Map::L * Map::F;   // floats per tile row in shared memory
+    constexpr int V = Map::kVec ? 4 : 1;
+    __shared__ int s_last;
+    const int n = p.n, nv = n / V, slots = H * nv;
+    const int tid = w * 32 + lane, nth = W * 32;
+    const int2 th = p.tile_heavy[tile];      // heavy id, ordinal
+    const int4 hv = p.heavy[th.x];           // panel, ws_base, ntiles
+    float* wsq = p.ws + (size_t)(hv.y + th.y) * H * n;
+    {   // the tile's item count and lead from its first slot (always an item)
+        const int a0 = p.item_aux[tile * W];
+        cnt = (a0 >> 8) & 0xff;
+        lead = a0 & 0xff;
+    }
+    for (int s = tid; s < slots; s += nth) {
+        const int r = s / nv, c = (s - r * nv) * V;
+        float a[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) a[v] = 0.f;
+        for (int q = 0; q < cnt; q++) {
+            const float* part = smem + (size_t)(lead + q) * WS + r * NR + c;
+#pragma unroll
+            for (int v = 0; v < V; v++) a[v] += part[v];
+        }
+        if constexpr (V == 4) __stcg(reinterpret_cast<float4*>(wsq + r * n + c), make_float4(a[0], a[1], a[2], a[3]));
+        else __stcg(wsq + r * n + c, a[0]);
+    }
+    // release/acquire through one thread (the CTA barrier orders the other
+    // threads' partial stores before thread 0's release, and thread 0's
+    // acquire before their loads): no per-thread fence.sc (__threadfence),
+    // whose latency under a full load of gathers cost ~35% of the kernel
+    asm volatile("bar.sync 1, %0;" :: "r"(nth) : "memory");
+    if (tid == 0) {
+        int old;
+        asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(old) : "l"(p.counters + th.x) : "memory");
+        s_last = old == hv.z - 1;
+        // the last arriver acquires (the non-last tiles skip the acquire's L1
+        // invalidation, which would evict the gathered B rows of every CTA on
+        // the SM)
+        if (s_last) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    asm volatile("bar.sync 1, %0;" :: "r"(nth) : "memory");
+    if (!s_last) return;
+    const float* base = p.ws + (size_t)hv.y * H * n;
+    for (int s = tid; s < slots; s += nth) {
+        const int r = s / nv, c = (s - r * nv) * V;
+        const int row = hv.x * H + r;
+        float a[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) a[v] = 0.f;
+        int t = 0;
+        for (; t + 4 <= hv.z; t += 4) {   // four tiles' loads in flight, summed in tile order
+            float q[4][V];
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const float* src = base + (size_t)(t + d) * H * n + r * n + c;
+                if constexpr (V == 4) {
+                    const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+                    q[d][0] = x.x; q[d][1] = x.y; q[d][2] = x.z; q[d][3] = x.w;
+                } else {
+                    q[d][0] = __ldcg(src);
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+#pragma unroll
+                for (int v = 0; v < V; v++) a[v] += q[d][v];
+        }
+        for (; t < hv.z; t++) {
+            const float* src = base + (size_t)t * H * n + r * n + c;
+#pragma unroll
+            for (int v = 0; v < V; v++) a[v] += __ldcg(src + v);
+        }
+        if (row < p.m) store_out<V, PP>(p, row, c, a);
+    }
+    if (tid == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
 }
 
 // One CTA tile.  Item slots are tile-major: tile t owns slots [t*W, t*W + W),
@@ -475,11 +693,12 @@ __host__ __device__ constexpr int warp_smem_floats() {
 // the panel's items in this tile).  Every warp of the CTA calls this; the
 // __syncthreads below is reached by all of them when the tile needs a combine
 // (the flag is tile-uniform).
-template <int H, class Map, int U, bool PROBE, class PP>
+template <int H, class Map, int U, int MODE, class PP>
 __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile, int w,
                                              int lane, int W) {
     constexpr int F = Map::F, S = Map::S, NR = Map::L * Map::F;   // NR: floats per tile row
-    constexpr int WS = warp_smem_floats<H, Map>();
+    constexpr bool PROBE = MODE == kProbe || MODE == kRecProbe;
+    constexpr int WS = warp_smem_floats<H, Map, MODE>();
     const int sub = lane / Map::L, lj = lane % Map::L;
     const int slot = tile * W + w;
     const int aux = p.item_aux[slot];
@@ -494,7 +713,9 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
 
     const int panel = it.x;
     if (active) {
-        if constexpr (H == 1) {
+        if constexpr (MODE >= kRec) {
+            walk_rec<H, Map, U, PROBE, PP>(p, it.y, it.z, acc, lane);
+        } else if constexpr (H == 1) {
             walk1<Map, U, PROBE, PP>(p, it.y, it.z, it.w, acc, lane);
         } else {
             walk<H, Map, U, PROBE, PP>(p, *reinterpret_cast<Stage<H>*>(smem + (size_t)w * WS), it.y,
@@ -511,6 +732,17 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
         }
     }
     __syncwarp();   // staging reads done before the area holds the partial
+#ifdef ESC_TEST_ATOMIC   // A/B experiment only: atomics into a pre-zeroed C instead of the combine
+    if constexpr (MODE == kRec) {
+        if (active && sub == 0)
+            for (int r = 0; r < H; r++)
+                if (panel * H + r < p.m)
+                    for (int v = 0; v < F / 4; v++)
+                        atomicAdd(reinterpret_cast<float4*>(p.C + (size_t)(panel * H + r) * p.n + Map::col(lj, 4 * v)),
+                                  make_float4(acc[r][4 * v], acc[r][4 * v + 1], acc[r][4 * v + 2], acc[r][4 * v + 3]));
+        return;
+    }
+#endif
 
     if constexpr (PROBE) {
         if (active) {
@@ -540,8 +772,12 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
                     }
         }
         __syncthreads();
+        if (heavy) {   // tile-uniform: every warp of a heavy tile combines (more barriers)
+            heavy_combine<H, Map, PP>(p, smem, tile, w, lane, W, cnt, lead, WS);
+            return;
+        }
         if (!active) return;
-        if (cnt == 1 && !heavy) {
+        if (cnt == 1) {
             store_rows<H, Map, PP>(p, panel, acc, sub, lj);
             return;
         }
@@ -563,61 +799,7 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
                         if (Map::kVec || j < n) acc[r][f] += part[r * NR + j];
                     }
         }
-        if (!heavy) {
-            store_rows<H, Map, PP>(p, panel, acc, sub, lj);
-            return;
-        }
-        // heavy panel: its tiles combine through the global workspace
-        const int2 th = p.tile_heavy[tile];      // heavy id, ordinal
-        const int4 hv = p.heavy[th.x];           // panel, ws_base, ntiles
-        float* wsq = p.ws + (size_t)(hv.y + th.y) * H * n;
-#pragma unroll
-        for (int r = 0; r < H; r++)
-            if ((r % S) == sub)
-#pragma unroll
-                for (int f = 0; f < F; f++) {
-                    const int j = Map::col(lj, f);
-                    if (Map::kVec || j < n) __stcg(wsq + r * n + j, acc[r][f]);
-                }
-        __threadfence();
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) last = (atomicAdd(p.counters + th.x, 1) == hv.z - 1);
-        last = __shfl_sync(kFull, last, 0);
-        if (!last) return;
-        __threadfence();
-#pragma unroll
-        for (int r = 0; r < H; r++)
-#pragma unroll
-            for (int f = 0; f < F; f++) acc[r][f] = 0.f;
-        // partials summed in tile order (deterministic); D tiles' loads in
-        // flight at once (the walk's registers are dead here; fewer for UFi > 1,
-        // whose H x F accumulators would otherwise set the kernel's register count)
-        constexpr int D = H == 1 ? (F <= 16 ? 4 : 2) : (H * F <= 8 ? 4 : H * F <= 16 ? 2 : 1);
-#pragma unroll 1
-        for (int t0 = 0; t0 < hv.z; t0 += D) {
-            float q[D][H][F];
-#pragma unroll
-            for (int d = 0; d < D; d++) {
-                const float* part = p.ws + (size_t)(hv.y + min(t0 + d, hv.z - 1)) * H * n;
-#pragma unroll
-                for (int r = 0; r < H; r++)
-#pragma unroll
-                    for (int f = 0; f < F; f++) {
-                        const int j = Map::col(lj, f);
-                        q[d][r][f] = ((r % S) == sub && (Map::kVec || j < n)) ? __ldcg(part + r * n + j) : 0.f;
-                    }
-            }
-#pragma unroll
-            for (int d = 0; d < D; d++)
-                if (t0 + d < hv.z)
-#pragma unroll
-                    for (int r = 0; r < H; r++)
-#pragma unroll
-                        for (int f = 0; f < F; f++) acc[r][f] += q[d][r][f];
-        }
-        store_rows<H, Map, PP>(p, hv.x, acc, sub, lj);
-        if (lane == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
+        store_rows<H, Map, PP>(p, panel, acc, sub, lj);
     }
 }
 
@@ -625,12 +807,38 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
 // measured and dropped: the hardware block scheduler already dispatches CTAs
 // dynamically, and the counter atomics and extra barriers cost 0.2-1.5 us per
 // launch on the latency-bound suite -- profiles/r1_notes.md.)
-template <int H, class Map, int U, bool PROBE>
-__global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_kernel(KParams p) {
+template <int H, class Map, int U, int MODE>
+__global__ void ESC_CSR_BOUNDS esc_spmm_kernel(KParams p) {
     extern __shared__ __align__(16) float smem[];
     grid_dep_launch();   // the next launch may start reading its plan
-    process_tile<H, Map, U, PROBE, KParams>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31,
-                                   blockDim.x >> 5);
+    process_tile<H, Map, U, MODE, KParams>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31,
+                                           blockDim.x >> 5);
+}
+
+// The record walk (kRec / kRecProbe) as its own kernel: its register budget
+// sets both the resident warps per SM and how many record / B-row loads ptxas
+// keeps in flight per warp -- the two quantities that decide a gather-bound,
+// latency-bound walk.  With "__launch_bounds__(512, 1)" ptxas takes all 128
+// registers (16 warps/SM); with "(512)" alone it settles near 55 and
+// interleaves each record's loads with the previous record's FMAs (4 loads in
+// flight); a register target of 72 keeps 8 loads in flight at 7 CTAs of 4
+// warps per SM: 512x4608@70% bCols 128, UFi 3: 24.6 us -> 19.1 us
+// (profiles/r2_notes.md, "record walk register target").
+#ifndef ESC_REC_MAXREG
+#define ESC_REC_MAXREG 72
+#endif
+#if ESC_REC_MAXREG > 0
+#define ESC_REC_BOUNDS __maxnreg__(ESC_REC_MAXREG)
+#else
+#define ESC_REC_BOUNDS __launch_bounds__(512)
+#endif
+template <int H, class Map, int U, int MODE>
+__global__ void ESC_REC_BOUNDS esc_rec_kernel(KParams p) {
+    static_assert(MODE == kRec || MODE == kRecProbe, "record modes only");
+    extern __shared__ __align__(16) float smem[];
+    grid_dep_launch();
+    process_tile<H, Map, U, MODE, KParams>(p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31,
+                                           blockDim.x >> 5);
 }
 
 using KernelFn = void (*)(KParams);
@@ -658,7 +866,7 @@ struct GProb {
     const float* vals;
     const float* B;
     float* C;
-    int m, n, W, packed;
+    int m, n, W;
     static constexpr bool kScatter = false;   // no fused all-gather in grouped launches
 };
 struct GroupParams {
@@ -668,7 +876,7 @@ struct GroupParams {
 };
 
 template <int H, class Map, int U>
-__global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_group_kernel(const __grid_constant__ GroupParams gp) {
+__global__ void ESC_CSR_BOUNDS esc_spmm_group_kernel(const __grid_constant__ GroupParams gp) {
     extern __shared__ __align__(16) float smem[];
     grid_dep_launch();
     const int t = blockIdx.x;
@@ -684,7 +892,7 @@ __global__ void __launch_bounds__(512, ESC_MINB) esc_spmm_group_kernel(const __g
         if ((q.item_aux[tile * q.W] >> 17) & 1) __syncthreads();
         return;
     }
-    process_tile<H, Map, U, false, GProb>(q, smem, tile, w, threadIdx.x & 31, q.W);
+    process_tile<H, Map, U, kCsr, GProb>(q, smem, tile, w, threadIdx.x & 31, q.W);
 }
 
 using GroupFn = void (*)(GroupParams);

@@ -14,6 +14,7 @@ struct Params {
     int cta_warps = 8;  // warps per CTA tile
     int variant = 1;    // 1 = vector (float4) lane map, 2 = scalar lane map
     int ufk = 4;        // B-row loads in flight per sub-warp step (UFk)
+    int packed = 0;     // 1: tuned for the packed-record walk (escs_spmm_packed)
     int colf = 0;       // B columns per lane of the vector map (bCols coarsening), 0 = default
     int tile_order = 0; // 0 auto, 1 panel order, 2 by longest item
     int nthreads = 0;   // planner threads
@@ -44,8 +45,10 @@ std::string validate_csr(int64_t m, int64_t k, int64_t nnz, const int32_t* rowpt
 void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                 const int32_t* colidx, int32_t bcols, const Params& p, PlanHost& out);
 
-// Auto parameters from the per-bCols table and the problem size.
-Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm);
+// Auto parameters from the per-bCols table and the problem size; h_req > 0
+// fixes UFi, packed selects the table of the record walk.
+Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm, int h_req = 0,
+                     bool packed = false);
 
 // Pick cta_warps from the item distribution and build the tile schedule.
 void build_tiles(PlanHost& ph, int cta_warps, bool by_length = true);
@@ -54,6 +57,7 @@ void build_tiles(PlanHost& ph, int cta_warps, bool by_length = true);
 struct DevPlan {
     const int32_t* gpk = nullptr;       // int32[G]: column | pattern << 27
     const int32_t* slot = nullptr;      // int32[nnz]
+    const int32_t* vbase = nullptr;     // int32[G]: slot of each gcol's first value (UFi > 1, escs_pack)
     const int32_t* items = nullptr;     // int4[n_slots]: panel, gcol_begin, gcol_end, slot_begin
     const int32_t* item_aux = nullptr;  // int32[n_slots]
     const int32_t* tile_heavy = nullptr;  // int2[n_tiles]
@@ -61,30 +65,34 @@ struct DevPlan {
     float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
     int32_t* counters = nullptr;        // int32[n_heavy]
     int m = 0, k = 0, nnz = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4, colf = 0;
+    int G = 0;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
 };
 
-// Launch the ESC SpMM kernel (one launch).  Returns a cudaError_t value.
+// Launch the ESC SpMM kernel (one launch).  packed: `vals` is the record
+// stream of escs_pack (record walk).  Returns a cudaError_t value.
 int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, void* stream,
                 bool vec_ok, bool packed = false, float* const* extra = nullptr,
                 int n_extra = 0, long long row_off = 0, bool multicast = false);
 // escs_spmm_group: n independent SpMMs, grouped into one launch per kernel
 // instance (UFi = 1 vector plans; the rest launch one by one).
 int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
-                 const float* const* B, float* const* C, void* stream, bool packed);
-// escs_pack: packed[s] = vals[slot[s]].
+                 const float* const* B, float* const* C, void* stream);
+// escs_pack: the record stream (packed_words(dp) int32 words).
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream);
-// Launch the gather probe (same walk, loads only).
-int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok);
+int64_t packed_words(const DevPlan& dp);
+// Launch the gather probe (same walk, loads only); packed != NULL: the record walk.
+int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok,
+                 const float* packed = nullptr);
 // Prepare kernel attributes (dynamic smem limits) once per plan.
 int prepare_kernels(DevPlan& dp);
-// Does a kernel instance exist for this configuration?
-bool kernel_supported(int h, int bcols, int variant, int ufk, int colf);
+// Does a kernel instance exist for this configuration (packed: the record walk)?
+bool kernel_supported(int h, int bcols, int variant, int ufk, int colf, bool packed = false);
 int default_colf(int bcols);
 int launch_spin(void* stream, long long cycles);   // tuner: busy-wait on the stream
-size_t smem_bytes(const DevPlan& dp);
+size_t smem_bytes(const DevPlan& dp, bool packed = false);
 // Resident CTAs per SM for this plan's launch configuration.
-int blocks_per_sm(const DevPlan& dp, bool vec, bool probe);
+int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed = false);
 
 }  // namespace escs

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -13,13 +14,40 @@
 namespace escs {
 
 namespace kern {
-// escs_pack: packed[s] = vals[slot[s]] (the paper's ANNZ, §3.3.3).
-__global__ void __launch_bounds__(256) esc_pack_kernel(const int* __restrict__ slot,
-                                                       const float* __restrict__ vals,
-                                                       float* __restrict__ out, int nnz) {
+// escs_pack: the record stream of the packed walk (esc_kernel.cuh "records";
+// the paper's value re-layout "ANNZ", §3.3.3).  One thread per gcol
+// j: UFi = 1 writes {col, vals[j]} (the slot map is the identity); UFi > 1
+// writes the gcol's packed word and its pattern rows' values by row, taking
+// the p = popcount(mask) values from slots vbase[j] .. vbase[j] + p - 1
+// (Reading R1: a gcol's values are contiguous in slot order, rows ascending).
+template <int H>
+__global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict__ gpk,
+                                                           const int* __restrict__ slot,
+                                                           const int* __restrict__ vbase,
+                                                           const float* __restrict__ vals,
+                                                           int* __restrict__ out, int G) {
+    constexpr int RW = RecFmt<H>::W;
     grid_dep_wait();
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nnz; s += gridDim.x * blockDim.x)
-        out[s] = vals[ld_stream(slot + s)];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < G; j += gridDim.x * blockDim.x) {
+        const int pk = gpk[j];
+        if constexpr (H == 1) {
+            *reinterpret_cast<int2*>(out + (size_t)j * 2) =
+                make_int2(pk & kColMask, __float_as_int(vals[j]));
+        } else {
+            int w[RW];
+#pragma unroll
+            for (int q = 0; q < RW; q++) w[q] = 0;
+            w[0] = pk;
+            const unsigned mk = (unsigned)pk >> kColBits;
+            int s = vbase[j];
+#pragma unroll
+            for (int r = 0; r < H; r++)
+                if ((mk >> r) & 1u) w[1 + r] = __float_as_int(vals[slot[s++]]);
+            int4* o = reinterpret_cast<int4*>(out + (size_t)j * RW);
+            o[0] = make_int4(w[0], w[1], w[2], w[3]);
+            if constexpr (RW == 8) o[1] = make_int4(w[4], w[5], w[6], w[7]);
+        }
+    }
 }
 
 // Busy-wait kernel for the plan-time tuner: occupies the stream while the
@@ -35,21 +63,26 @@ __global__ void spin_kernel(long long cycles) {
 
 namespace {
 
-kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, bool probe, int colf) {
-    if (vec) return kern::get_vec(n, colf > 0 ? colf : kern::default_colf(n), h, ufk, probe);
-    if (probe) return nullptr;
+kern::KernelFn select_kernel(int h, int n, bool vec, int ufk, int mode, int colf) {
+    if (vec) {
+        kern::KernelFn f = kern::get_vec(n, colf > 0 ? colf : kern::default_colf(n), h, ufk, mode);
+        // the CSR walk has the alternative coarsening factors at UFi = 1 only:
+        // a record-tuned plan (UFi > 1, colf != default) runs escs_spmm on the
+        // default lane map (same output layout, same per-warp smem)
+        if (!f && mode < kern::kRec) f = kern::get_vec(n, kern::default_colf(n), h, ufk, mode);
+        return f;
+    }
+    if (mode != kern::kCsr) return nullptr;   // probes and records: vector maps only
     if (ufk < 2) ufk = 2;   // the scalar map has UFk 2/4/8 instances
-    if (n <= 32) return kern::get_s1(h, ufk, false);
-    if (n <= 64) return kern::get_s2(h, ufk, false);
-    if (n <= 128) return kern::get_s4(h, ufk, false);
-    if (n <= 256) return kern::get_s8(h, ufk, false);
+    if (n <= 32) return kern::get_s1(h, ufk, mode);
+    if (n <= 64) return kern::get_s2(h, ufk, mode);
+    if (n <= 128) return kern::get_s4(h, ufk, mode);
+    if (n <= 256) return kern::get_s8(h, ufk, mode);
     return nullptr;
 }
 
-kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C,
-                          bool packed = false) {
+kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, float* C) {
     kern::KParams p = {};
-    p.packed = packed ? 1 : 0;
     p.gpk = dp.gpk;
     p.slot = dp.slot;
     p.items = reinterpret_cast<const int4*>(dp.items);
@@ -81,7 +114,10 @@ int launch(kern::KernelFn fn, const DevPlan& dp, const kern::KParams& p, size_t 
     cfg.attrs = attr;
     cfg.numAttrs = dp.pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, fn, p);
-    if (e != cudaSuccess) return (int)e;
+    if (e != cudaSuccess) {
+        cudaGetLastError();   // consume it: a refused launch must not fail the next one
+        return (int)e;
+    }
     return (int)cudaGetLastError();
 }
 
@@ -94,10 +130,12 @@ int launch_spin(void* stream, long long cycles) {
     return (int)cudaGetLastError();
 }
 
-bool kernel_supported(int h, int bcols, int variant, int ufk, int colf) {
+bool kernel_supported(int h, int bcols, int variant, int ufk, int colf, bool packed) {
     if (h < 1 || h > 4 || bcols < 1 || bcols > 256) return false;
-    return select_kernel(h, bcols, variant == 1, ufk, false, colf) != nullptr &&
-           select_kernel(h, bcols, false, ufk, false, 0) != nullptr;
+    if (packed)   // the record walk: vector lane map only
+        return variant == 1 && select_kernel(h, bcols, true, ufk, kern::kRec, colf) != nullptr;
+    return select_kernel(h, bcols, variant == 1, ufk, kern::kCsr, colf) != nullptr &&
+           select_kernel(h, bcols, false, ufk, kern::kCsr, 0) != nullptr;
 }
 
 // floats per lane-column slot F of the lane map the launch will use
@@ -106,59 +144,82 @@ static int lane_floats(int n, bool vec) {
     return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8;
 }
 
-static size_t smem_for(const DevPlan& dp, bool vec) {
+// Dynamic shared memory of a launch: W warps x the kernel's per-warp area
+// (esc_kernel.cuh warp_smem_floats: the CSR walk's staging area at UFi > 1
+// and the H x bCols combine partial share it; the record walk needs only the
+// partial).
+static size_t smem_for(const DevPlan& dp, bool vec, bool rec = false) {
     const int F = lane_floats(dp.bcols, vec);
     const int hp = dp.h == 3 ? 4 : dp.h;
-    const size_t stage = (size_t)2 * 32 * (1 + hp);           // Stage<H> floats
-    const size_t part = (size_t)dp.h * 32 * F;   // kernel strides warps by max(stage, part)
+    const size_t stage = (!rec && dp.h > 1) ? (size_t)2 * 32 * (1 + hp) : 0;   // Stage<H> floats
+    const size_t part = (size_t)dp.h * 32 * F;
     return (size_t)dp.cta_warps * (stage > part ? stage : part) * sizeof(float);
 }
 
-size_t smem_bytes(const DevPlan& dp) { return smem_for(dp, dp.variant == 1); }
+size_t smem_bytes(const DevPlan& dp, bool packed) { return smem_for(dp, dp.variant == 1, packed); }
+
+// Kernel attributes are per function and shared by every plan: only ever
+// raise the dynamic shared memory limit (never lower it under another plan);
+// the read-and-raise is serialised so concurrent planners cannot lower it.
+static std::mutex g_attr_mutex;
+static int raise_smem(kern::KernelFn fn, size_t smem) {
+    if (!fn || smem <= 32 * 1024) return 0;   // well under the 48 KB default (static smem included)
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    cudaFuncAttributes attr;
+    cudaError_t e = cudaFuncGetAttributes(&attr, (const void*)fn);
+    if (e != cudaSuccess) return (int)e;
+    if ((size_t)attr.maxDynamicSharedSizeBytes >= smem) return 0;
+    return (int)cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
+}
 
 int prepare_kernels(DevPlan& dp) {
-    // Kernel attributes are per function and shared by every plan: only ever
-    // raise the dynamic shared memory limit (never lower it under another plan).
     for (int vec = 0; vec < 2; vec++) {
         if (vec && dp.variant != 1) continue;
-        const size_t smem = smem_for(dp, vec == 1);
-        if (smem <= 48 * 1024) continue;
-        kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec == 1, dp.ufk, false, vec ? dp.colf : 0);
-        if (!fn) continue;
-        cudaFuncAttributes attr;
-        cudaError_t e = cudaFuncGetAttributes(&attr, (const void*)fn);
-        if (e != cudaSuccess) return (int)e;
-        if ((size_t)attr.maxDynamicSharedSizeBytes >= smem) continue;
-        e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        if (vec) {
-            kern::KernelFn pf = select_kernel(dp.h, dp.bcols, true, dp.ufk, true, dp.colf);
-            if (pf) cudaFuncSetAttribute((const void*)pf,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int colf = vec ? dp.colf : 0;
+        const int modes[4] = {kern::kCsr, kern::kProbe, kern::kRec, kern::kRecProbe};
+        for (int md : modes) {
+            const bool rec = md >= kern::kRec;
+            if (rec && !vec) continue;
+            if (int e = raise_smem(select_kernel(dp.h, dp.bcols, vec == 1, dp.ufk, md, colf),
+                                   smem_for(dp, vec == 1, rec)))
+                return e;
         }
     }
     return 0;
 }
 
-int blocks_per_sm(const DevPlan& dp, bool vec, bool probe) {
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, probe, vec ? dp.colf : 0);
+int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed) {
+    const int mode = packed ? (probe ? kern::kRecProbe : kern::kRec) : (probe ? kern::kProbe : kern::kCsr);
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, mode, vec ? dp.colf : 0);
     if (!fn) return 1;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn, 32 * dp.cta_warps,
-                                                      smem_for(dp, vec)) != cudaSuccess) {
+                                                      smem_for(dp, vec, packed)) != cudaSuccess) {
         cudaGetLastError();
         return 1;
     }
     return nb > 0 ? nb : 1;
 }
 
+int64_t packed_words(const DevPlan& dp) {
+    const int rw = dp.h == 1 ? 2 : (dp.h <= 3 ? 4 : 8);
+    return (int64_t)dp.G * rw;
+}
+
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream) {
-    if (dp.nnz == 0) return 0;
+    if (dp.G == 0) return 0;
     const int threads = 256;
-    const int blocks = (int)std::min<long>(((long)dp.nnz + threads - 1) / threads, 148L * 16);
-    kern::esc_pack_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(dp.slot, vals, packed,
-                                                                          dp.nnz);
+    const int blocks = (int)std::min<long>(((long)dp.G + threads - 1) / threads, 148L * 16);
+    int* out = reinterpret_cast<int*>(packed);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dp.h) {
+        case 1: kern::esc_pack_rec_kernel<1><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        default: return (int)cudaErrorInvalidConfiguration;
+    }
     return (int)cudaGetLastError();
 }
 
@@ -166,19 +227,21 @@ int launch_spmm(const DevPlan& dp, const float* vals, const float* B, float* C, 
                 bool vec_ok, bool packed, float* const* extra, int n_extra, long long row_off,
                 bool multicast) {
     const bool vec = vec_ok && dp.variant == 1;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, false, vec ? dp.colf : 0);
+    if (packed && !vec) return (int)cudaErrorInvalidConfiguration;   // records: vector map only
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, vec, dp.ufk, packed ? kern::kRec : kern::kCsr,
+                                      vec ? dp.colf : 0);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
-    kern::KParams p = make_params(dp, vals, B, C, packed);
+    kern::KParams p = make_params(dp, vals, B, C);
     p.n_extra = n_extra;
     p.mc = multicast ? 1 : 0;
     p.row_off = row_off;
     for (int d = 0; d < n_extra && d < kern::kMaxScatter; d++) p.extra[d] = extra[d];
-    return launch(fn, dp, p, smem_for(dp, vec), stream);
+    return launch(fn, dp, p, smem_for(dp, vec, packed), stream);
 }
 
 int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
-                 const float* const* B, float* const* C, void* stream, bool packed) {
+                 const float* const* B, float* const* C, void* stream) {
     auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
     // problems with a grouped instance (UFi = 1, vector map, aligned B/C),
     // keyed by kernel; everything else launches on its own, in input order
@@ -188,11 +251,11 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
         if (dp.n_tiles == 0) continue;
         const bool vec = dp.variant == 1 && al16(B[i]) && al16(C[i]);
         kern::GroupFn g = nullptr;
-        if (vec && dp.h == 1 && smem_for(dp, true) <= 48 * 1024)
+        if (vec && dp.h == 1 && smem_for(dp, true) <= 32 * 1024)   // no attribute raise for group kernels
             g = kern::get_vec_group(dp.bcols, dp.colf > 0 ? dp.colf : kern::default_colf(dp.bcols),
                                     dp.ufk);
         if (!g) {
-            const int e = launch_spmm(dp, vals[i], B[i], C[i], stream, vec, packed);
+            const int e = launch_spmm(dp, vals[i], B[i], C[i], stream, vec, false);
             if (e) return e;
             continue;
         }
@@ -231,7 +294,6 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
             q.m = dp.m;
             q.n = dp.bcols;
             q.W = dp.cta_warps;
-            q.packed = packed ? 1 : 0;
             gp.tile_start[j - a] = tiles;
             tiles += dp.n_tiles;
             maxw = std::max(maxw, dp.cta_warps);
@@ -250,7 +312,10 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
         cudaError_t e = cudaLaunchKernelEx(&cfg, keyed[a].first, gp);
-        if (e != cudaSuccess) return (int)e;
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return (int)e;
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess) return (int)e;
         a = b;
@@ -258,13 +323,16 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
     return 0;
 }
 
-int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok) {
+int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok,
+                 const float* packed) {
     if (!(vec_ok && dp.variant == 1)) return (int)cudaErrorInvalidConfiguration;
-    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, true, dp.ufk, true, dp.colf);
+    const bool rec = packed != nullptr;
+    kern::KernelFn fn = select_kernel(dp.h, dp.bcols, true, dp.ufk, rec ? kern::kRecProbe : kern::kProbe,
+                                      dp.colf);
     if (!fn) return (int)cudaErrorInvalidConfiguration;
     if (dp.n_tiles == 0) return 0;
-    kern::KParams p = make_params(dp, nullptr, B, sink);
-    return launch(fn, dp, p, smem_for(dp, true), stream);
+    kern::KParams p = make_params(dp, packed, B, sink);
+    return launch(fn, dp, p, smem_for(dp, true, rec), stream);
 }
 
 }  // namespace escs

@@ -257,8 +257,12 @@ void build_tiles(PlanHost& ph, int W, bool by_length) {
                 ph.slot_aux.push_back(lc[its[k]] | (1 << 16) | (sync ? 1 << 17 : 0) |
                                       (hid >= 0 ? 1 << 18 : 0));
             } else {
+                // empty slot: inactive; in a heavy tile it still carries the
+                // tile's heavy flag and item count (all warps of a heavy tile
+                // take part in its combine, esc_kernel.cuh heavy_combine)
                 ph.slot_item.push_back(-1);
-                ph.slot_aux.push_back(sync ? 1 << 17 : 0);
+                ph.slot_aux.push_back((sync ? 1 << 17 : 0) |
+                                      (hid >= 0 ? (1 << 18) | ((int32_t)its.size() << 8) : 0));
             }
         }
         ph.tile_heavy.push_back(hid);
@@ -329,23 +333,28 @@ void build_tiles(PlanHost& ph, int W, bool by_length) {
 }
 
 // Parameter table (§3.5 Scheduler & Tuner), fitted to the
-// profiling sweeps of tools/tune.py on B200 (profiles/r1_tune_*.json):
-//  * UFi: the sweep over {1, 2, 4} on both layer suites picks UFi = 1 for every
-//    case (UFi = 4 is 1.1-1.9x slower): the B rows that enumeration saves
-//    (p = h(1-s)/(1-s^h) = 1.58 at 70%) hit the 126 MB L2 / large L1 anyway,
-//    while patterns add the slot indirection and predicated rows.  Explicit
-//    UFi (escs_plan_ex / ESCS_PARAMS) runs the enumerated kernel.
+// profiling sweeps of tools/tune.py on B200 (profiles/r1_tune_*.json,
+// profiles/r2_notes.md):
+//  * UFi, CSR-value walk (escs_spmm): UFi = 1 -- every pattern row costs a
+//    slot-map indirection and staged values, which outweighs the B rows the
+//    enumeration saves (r1 sweeps).  Packed-record walk (escs_spmm_packed,
+//    packed = 1): the record carries the column, the pattern and the row values
+//    in one broadcast load, so the p = h(1-s)/(1-s^h) B-row reuse of the
+//    enumeration pays where p is large: UFi 4 below 75% sparsity, 2 below 85%,
+//    1 above (the plan-time tuner searches UFi 1..4 either way).
 //  * UFk = 8 B rows in flight per sub-warp on the layer suites; 4 on large
 //    problems (occupancy) and at bCols 256 (registers).
 //  * T: about 1536 items per launch (~10 warps per SM on 148 SMs: each item
 //    long enough to amortise its dependent round trips), at least 16 columns,
 //    rounded (with a 3-sigma margin on the panel stream) so that a typical
 //    panel splits into equal items.
-Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm) {
+Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm, int h_req,
+                     bool packed) {
     Params p;
     const double d = (double)nnz / ((double)m * (double)k);
     const double s = 1.0 - d;
-    p.h = 1;
+    p.packed = packed ? 1 : 0;
+    p.h = h_req > 0 ? h_req : (!packed ? 1 : s < 0.75 ? 4 : s < 0.85 ? 2 : 1);
     p.variant = (bcols == 4 || bcols == 8 || bcols == 16 || bcols == 32 || bcols == 64 ||
                  bcols == 128 || bcols == 256) ? 1 : 2;
     // more rows in flight per warp on the small, latency-bound layers; more
@@ -357,8 +366,10 @@ Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm)
     // bCols coarsening (columns per lane): on the large L1-wavefront-bound
     // problems a 16-column register tile per lane (8 lanes per B row, 4 rows
     // per warp instruction) halves the per-row broadcasts and issue
-    // (C4: 91.5 -> 83.6 us hot-L2, C5: 2.25 -> 2.14 ms; profiles/r1_notes.md)
-    p.colf = (bcols == 128 && g_est > 1.5e6) ? 16 : 0;
+    // (C4: 91.5 -> 83.6 us hot-L2, C5: 2.25 -> 2.14 ms; profiles/r1_notes.md);
+    // the packed walk takes 8 columns per lane at bCols 128 (two records per
+    // warp load instruction; exp sweeps in profiles/r2_notes.md)
+    p.colf = (bcols == 128 && g_est > 1.5e6) ? 16 : (packed && bcols == 128) ? 8 : 0;
     const double sp = (double)k * (1.0 - std::pow(s, p.h));   // expected panel stream
     const double G = std::ceil((double)m / p.h) * sp;
     const double target_items = 1536.0 * (double)n_sm / 148.0;

@@ -22,7 +22,8 @@ PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "s
                "item_panel", "item_group_begin", "item_gcol_ptr")
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
                     "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
-                    "escs_pack", "escs_spmm_packed", "escs_spmm_scatter", "escs_spmm_group")
+                    "escs_pack", "escs_spmm_packed", "escs_spmm_scatter", "escs_spmm_group",
+                    "escs_gather_probe_packed")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -36,7 +37,7 @@ class _Params(ctypes.Structure):
                 ("cta_warps", ctypes.c_int32), ("variant", ctypes.c_int32), ("ufk", ctypes.c_int32),
                 ("nthreads", ctypes.c_int32), ("autotune", ctypes.c_int32),
                 ("colf", ctypes.c_int32), ("tile_order", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("packed", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _View(ctypes.Structure):
@@ -51,7 +52,8 @@ class _Stats(ctypes.Structure):
                                               "workspace_bytes")] + \
                [("plan_seconds", ctypes.c_double), ("ctas_per_sm", ctypes.c_int32),
                 ("autotuned", ctypes.c_int32), ("colf", ctypes.c_int32),
-                ("tile_order", ctypes.c_int32)]
+                ("tile_order", ctypes.c_int32), ("pdl", ctypes.c_int32), ("packed", ctypes.c_int32),
+                ("packed_words", ctypes.c_int64)]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -73,6 +75,8 @@ _lib.escs_pack.argtypes = [_vp, _vp, _vp, _vp]
 _lib.escs_pack.restype = ctypes.c_int
 _lib.escs_gather_probe.argtypes = [_vp, _vp, _vp, _vp]
 _lib.escs_gather_probe.restype = ctypes.c_int
+_lib.escs_gather_probe_packed.argtypes = [_vp, _vp, _vp, _vp, _vp]
+_lib.escs_gather_probe_packed.restype = ctypes.c_int
 _lib.escs_free.argtypes = [_vp]
 _lib.escs_free.restype = None
 _lib.escs_last_error.argtypes = [ctypes.POINTER(ctypes.c_char_p)]
@@ -149,13 +153,15 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
-                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0) -> Plan:
+                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0, packed=0) -> Plan:
     """escs_plan with explicit escs_params (include/escs.h); 0 = auto for every
     field.  autotune: 1 = latency objective (one stream), 2 = concurrent
-    throughput objective (independent SpMMs overlapped on several streams)."""
+    throughput objective (independent SpMMs overlapped on several streams).
+    packed=1: plan (and tune, including UFi) for escs_pack + escs_spmm_packed."""
     rowptr, colidx = _csr_args(rowptr, colidx)
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
-                int(nthreads), int(autotune), int(colf), int(tile_order), (ctypes.c_int32 * 2)())
+                int(nthreads), int(autotune), int(colf), int(tile_order), int(packed),
+                (ctypes.c_int32 * 1)())
     h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
                           int(bCols), ctypes.byref(p))
     if not h:
@@ -234,15 +240,24 @@ def escs_spmm_group(plans, vals, B, C, stream=None) -> None:
     Group(plans, vals, B, C)(stream)
 
 
-def escs_pack(plan: Plan, vals, packed, stream=None) -> None:
-    """packed[s] = vals[slot_src[s]] on the device (the paper's ANNZ)."""
+def escs_pack(plan: Plan, vals, packed=None, stream=None):
+    """Write the plan's record stream (include/escs.h escs_pack) from the CSR
+    values; allocates it (a torch int32 CUDA tensor of
+    escs_plan_stats.packed_words) when `packed` is None.  Returns `packed`."""
+    if packed is None:
+        import torch
+        dev = vals.device if not isinstance(vals, int) else torch.device("cuda")
+        packed = torch.empty(max(int(plan.info["packed_words"]), 4), dtype=torch.int32, device=dev)
+    elif not isinstance(packed, int) and packed.numel() < int(plan.info["packed_words"]):
+        raise EscsError(ESCS_ERR_ARG, f"packed needs {plan.info['packed_words']} words")
     rc = _lib.escs_pack(plan.handle, _ptr(vals), _ptr(packed), _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
+    return packed
 
 
 def escs_spmm_packed(plan: Plan, packed, B, C, stream=None) -> None:
-    """C = A x B with values pre-packed by escs_pack."""
+    """C = A x B from the record stream written by escs_pack."""
     rc = _lib.escs_spmm_packed(plan.handle, _ptr(packed), _ptr(B), _ptr(C), _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
@@ -265,6 +280,13 @@ def escs_spmm_scatter(plan: Plan, vals, B, dsts, row_offset: int, stream=None,
 
 def escs_gather_probe(plan: Plan, B, sink, stream=None) -> None:
     rc = _lib.escs_gather_probe(plan.handle, _ptr(B), _ptr(sink), _stream_ptr(stream))
+    if rc != ESCS_OK:
+        _raise_last()
+
+
+def escs_gather_probe_packed(plan: Plan, packed, B, sink, stream=None) -> None:
+    rc = _lib.escs_gather_probe_packed(plan.handle, _ptr(packed), _ptr(B), _ptr(sink),
+                                       _stream_ptr(stream))
     if rc != ESCS_OK:
         _raise_last()
 

@@ -270,30 +270,6 @@ def test_pdl_stream_order_with_neighbours(torch_cuda):
         assert np.array_equal(c.cpu().numpy().astype(np.float64), ref * (it + 1))
 
 
-@pytest.mark.parametrize("ufi", [1, 2, 4])
-def test_pack_then_packed_spmm_bitwise(torch_cuda, ufi):
-    """escs_pack (the paper's ANNZ, values in slot order) + escs_spmm_packed
-    gives bitwise the same C as escs_spmm on CSR-ordered values, and the
-    packed array is exactly vals[slot_src]."""
-    torch = torch_cuda
-    from paper_2506_15174_b200 import escs
-    A = synth.magnitude_pruned(512, 768, 0.8, 31 + ufi)
-    B = synth.dense_b(768, 64, 5)
-    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, ufi=ufi, T=40)
-    dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
-    packed = torch.empty_like(dv)
-    escs.escs_pack(pl, dv, packed)
-    C1 = torch.empty(A.m, 64, device="cuda")
-    C2 = torch.empty(A.m, 64, device="cuda")
-    escs.escs_spmm(pl, dv, dB, C1)
-    escs.escs_spmm_packed(pl, packed, dB, C2)
-    torch.cuda.synchronize()
-    slot = pl.export()["slot_src"]
-    assert np.array_equal(packed.cpu().numpy(), A.vals[slot])
-    assert torch.equal(C1, C2)
-    check_tol(A, B, C2.cpu().numpy())
-
-
 def test_autotuned_plan_parity(torch_cuda):
     """An autotuned plan is still the canonical plan of its (UFi, T) -- byte
     identical to the oracle partitioner given that header -- and exact."""

@@ -45,13 +45,13 @@ def main():
         ok = np.array_equal(C.cpu().numpy().astype(np.float64), ref)
         print(n, prm, "ok" if ok else "MISMATCH", flush=True)
         bad += not ok
-    # values pre-packed by escs_pack (the paper's ANNZ), UFi 4, long items
+    # the packed record walk (escs_pack + escs_spmm_packed), UFi 4, long items,
+    # heavy panels through the workspace
     Ad, B = synth.dyadic_twin(W, 64, 8)
-    pl = escs.escs_plan_ex(W.m, W.k, W.nnz, W.rowptr, W.colidx, 64, ufi=4, T=300, cta_warps=4)
+    pl = escs.escs_plan_ex(W.m, W.k, W.nnz, W.rowptr, W.colidx, 64, ufi=4, T=300, cta_warps=4, packed=1)
     dv = torch.from_numpy(Ad.vals).cuda()
-    pk = torch.empty_like(dv)
     C = torch.empty(W.m, 64, device="cuda")
-    escs.escs_pack(pl, dv, pk)
+    pk = escs.escs_pack(pl, dv)
     escs.escs_spmm_packed(pl, pk, torch.from_numpy(B).cuda(), C)
     torch.cuda.synchronize()
     ok = np.array_equal(C.cpu().numpy().astype(np.float64),

@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--warps", default="0")
     ap.add_argument("--colf", default="0", help="B columns per lane of the vector map (0 = default)")
     ap.add_argument("--filter", default="", help="comma-separated substrings of case names")
-    ap.add_argument("--packed", action="store_true", help="time escs_spmm_packed (values pre-packed)")
+    ap.add_argument("--packed", action="store_true", help="time escs_spmm_packed (the record walk on escs_pack's stream)")
     a = ap.parse_args()
     import torch
     import bench
@@ -57,12 +57,12 @@ def main():
         for ufi, ufk, T, w, cf in grid:
             try:
                 pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n,
-                                       ufi=ufi, ufk=ufk, T=T, cta_warps=w, colf=cf)
+                                       ufi=ufi, ufk=ufk, T=T, cta_warps=w, colf=cf,
+                                       packed=1 if a.packed else 0)
             except escs.EscsError:
                 continue
             if a.packed:
-                pv = torch.empty_like(dv)
-                escs.escs_pack(pl, dv, pv, stream)
+                pv = escs.escs_pack(pl, dv, None, stream)
                 fn = lambda: escs.escs_spmm_packed(pl, pv, dB, dC, stream)
             else:
                 fn = lambda: escs.escs_spmm(pl, dv, dB, dC, stream)
