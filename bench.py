@@ -2,22 +2,26 @@
 """Benchmark of the ESC SpMM hot path (arXiv 2506.15174) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl escs|reference]
-                    [--workload transformer|resnet|suite|c1|c4|c5] [--no-compare]
+                    [--workload suite|transformer|resnet|resnet50|c1|c4|c5]
+                    [--csr] [--ufi U] [--no-compare] [--streams S]
 
-A *step* is one pass of the whole hot path over the workload: one
-``escs_spmm`` (one kernel launch) per problem of the workload with inputs
-resident in HBM.  Default workload: the layer suite BASELINE.json's metric
-(geomean over "the sparse ResNet-50/Transformer layer suite at bCols
-32/64/128") is quoted on -- configs[1] Transformer {512x512, 2048x512,
-512x2048} + configs[2] ResNet-50 im2col {256x2304, 512x4608, 2048x512}, each
-at {70,80,90,95,98}% x bCols {32,64,128} = 90 SpMMs per step.  With N>1 ranks (torchrun), every
-problem is row-block sharded (rank r owns rows [r*m/N, (r+1)*m/N), B
-replicated, no collective on the hot path): total work is
-fixed, so scaling is "strong".  The independent problems of a suite run on
---streams S streams (default 16, LPT by flops; forked from and joined into the
-timed stream) on plans autotuned for concurrent throughput (escs_params.autotune
-= 2); the same steps on one stream, on the latency-autotuned plans, are
-reported as "serial".
+A *step* is one pass of the whole hot path over the workload: every problem's
+SpMM, one kernel launch each, inputs resident in HBM.  Default workload: the
+layer suite BASELINE.json's metric (geomean over "the sparse
+ResNet-50/Transformer layer suite at bCols 32/64/128") is quoted on --
+configs[1] Transformer {512x512, 2048x512, 512x2048} + configs[2] ResNet-50
+im2col {256x2304, 512x4608, 2048x512}, each at {70,80,90,95,98}% x bCols
+{32,64,128} = 90 SpMMs per step.
+
+Path: each weight matrix is planned once (escs_plan_ex, autotuned for the
+packed record walk, UFi searched 1..4) and transformed once (escs_pack, the
+paper's data transformation); a step is escs_spmm_packed per layer
+on ONE stream (`value`).  `--csr` times escs_spmm on the CSR values instead;
+`--ufi 4` forces the enumerated path.  The same plans on --streams S streams
+(layers LPT-partitioned) are reported beside it with cuSPARSE on the same
+streams.  With N>1 ranks (torchrun) a suite is partitioned over ranks by
+problem (LPT, no collective); a single large problem is row-block sharded
+(SURVEY §8(e)).
 
 Timing: W untimed warm-up steps, then K timed steps.  Before each step the L2
 is flushed by writing a 256 MiB buffer (> 126 MB L2), and a device-side sleep
@@ -25,8 +29,10 @@ is queued so that the host enqueues the whole step ahead of the GPU; the step
 itself is bracketed by CUDA events on the launching stream (flush and sleep
 are outside the events).  Barrier + synchronize on both sides; max over ranks.
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
-(fp64, oracle/) on the same workload instead (the tier's reference arm).
+Prints ONE JSON line (rank 0), with the per-case table (hot L2, SURVEY §8(d)
+roofline bounds per case) when --no-compare is not given.  ``--impl
+reference`` times the CPU oracle (fp64, oracle/) on the same workload instead
+(the tier's reference arm).
 """
 from __future__ import annotations
 
@@ -60,12 +66,14 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
 
 
-def committed_traffic(workload_name):
-    """DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+def committed_traffic(workload_name, case=None):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json: {"workload", "case", "dram_bytes_per_launch",
+    "source"}); None when the committed capture is for another workload/case."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
-        if t.get("workload") == workload_name:
+        if t.get("workload") == workload_name and (case is None or t.get("case") in (None, case)):
             return t["dram_bytes_per_launch"], t["source"]
     except Exception:
         pass
@@ -152,13 +160,36 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- reference arm
 
+def _oracle_native():
+    """The oracle as the CPU baseline: built -O3 -march=native on this host."""
+    import oracle
+    lib = oracle.use_native()
+    return oracle, os.path.basename(lib)
+
+
 def oracle_time(problems, budget_s=10.0, max_reps=1000):
     """Time the fp64 CPU oracle over the whole workload (repeated until about
-    budget_s of CPU work).  Returns (GFLOP/s, reps, seconds, threads)."""
-    import oracle
+    budget_s of CPU work; a bounded sample of one repetition for workloads
+    whose single pass exceeds the budget).  Returns (GFLOP/s, reps, seconds,
+    threads, sample description)."""
+    oracle, _ = _oracle_native()
     threads = os.cpu_count() or 1
     flops = sum(p.flops for p in problems)
     reps, t_total = 0, 0.0
+    if len(problems) == 1 and problems[0].A.nnz > 20_000_000:
+        # one huge problem (C5): time a bounded row sample (the oracle's work
+        # is linear in the rows it computes)
+        p = problems[0]
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(p.A.m, p.A.m // 16, replace=False))
+        nnz_s = int(np.sum(np.diff(p.A.rowptr)[rows]))
+        while reps < 3 and t_total < budget_s:
+            t0 = time.perf_counter()
+            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, rows=rows, nthreads=threads)
+            t_total += time.perf_counter() - t0
+            reps += 1
+        return (2 * nnz_s * p.bcols * reps / t_total / 1e9, reps, t_total, threads,
+                f"{rows.size} random rows of {p.name} (1/16 of the rows) x{reps}")
     while reps < max_reps and t_total < budget_s:
         t0 = time.perf_counter()
         for p in problems:
@@ -166,7 +197,27 @@ def oracle_time(problems, budget_s=10.0, max_reps=1000):
             oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, p.B, nthreads=threads)
         t_total += time.perf_counter() - t0
         reps += 1
-    return flops * reps / t_total / 1e9, reps, t_total, threads
+    return flops * reps / t_total / 1e9, reps, t_total, threads, f"whole workload x{reps}"
+
+
+def oracle_c1_single_thread(reps=200):
+    """C1 (256x256 @ 90%, bCols 32) on ONE thread (SURVEY §8(d) oracle timing)."""
+    oracle, _ = _oracle_native()
+    from paper_2506_15174_b200 import synth
+    p = synth.config("c1")
+    A = p.A
+    oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, p.B, nthreads=1)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, p.B, nthreads=1)
+    dt = (time.perf_counter() - t0) / reps
+    return {"us_per_call": dt * 1e6, "gflops": p.flops / dt / 1e9, "reps": reps, "threads": 1}
+
+
+def cpu_info(threads):
+    import oracle
+    return {"cpu_model": oracle.cpu_model(), "nproc": os.cpu_count(), "threads": threads,
+            "build": "gcc -O3 -march=native -ffp-contract=off -fopenmp (oracle/escs_oracle.c)"}
 
 
 def run_reference(args):
@@ -174,29 +225,39 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    import oracle
+    oracle, _ = _oracle_native()
     problems, desc = workload(args.workload)
     threads = os.cpu_count() or 1
     flops = sum(p.flops for p in problems)
-    for _ in range(args.warmup):
+    big = len(problems) == 1 and problems[0].A.nnz > 20_000_000
+    rows = None
+    if big:   # bounded sample per step: 1/16 of C5's rows (same metric: GFLOP/s)
+        p = problems[0]
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(p.A.m, p.A.m // 16, replace=False))
+        flops = 2 * int(np.sum(np.diff(p.A.rowptr)[rows])) * p.bcols
+
+    def one():
         for p in problems:
-            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, nthreads=threads)
+            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, rows=rows, nthreads=threads)
+    for _ in range(args.warmup):
+        one()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        for p in problems:
-            oracle.spmm(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, p.A.vals, p.B, nthreads=threads)
+        one()
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = flops * args.steps / tot / 1e9
-    sample = f"whole workload ({len(problems)} SpMMs) per step, fp64 C oracle, OpenMP over rows"
+    sample = (f"whole workload ({len(problems)} SpMMs) per step" if rows is None else
+              f"{rows.size} random rows of {problems[0].name} per step") + ", fp64 C oracle, OpenMP over rows"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc, "problems": len(problems)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                              "sample": sample}, **cpu_info(threads)),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -248,39 +309,29 @@ def graph_time(torch, fn, stream, min_ms=2.0, reps=11, stats=None):
     return statistics.median(ts)
 
 
-def gather_ceiling(torch, dev, stream, n_sm):
-    """Measured B-row gather ceiling (GB/s): bl_gather_peak gathers pseudo-
-    random 512-byte rows of a 64 MiB L2-resident B (C5's B) with no index
-    loads, values or FMAs; best of 6 lane maps / depths, 64 warps per SM."""
-    import ctypes
-    from paper_2506_15174_b200.build import BENCH_LIB
-    bl = ctypes.CDLL(BENCH_LIB)
-    bl.bl_gather_peak.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                  ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
-    k = 131072
-    B = torch.rand(k, 128, device=dev)
-    sink = torch.zeros(256, device=dev)
-    ctas, rpw = n_sm * 8, 2048
-    rows = ctas * 8 * rpw
-    best = None
-    for v in range(6):
-        for _ in range(2):
-            assert bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream) == 0
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(3):
-            bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream)
-        b.record(stream)
-        b.synchronize()
-        gbs = 3 * rows * 512 / (a.elapsed_time(b) * 1e-3) / 1e9
-        best = gbs if best is None else max(best, gbs)
-    del B
-    return best
+def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs):
+    """SURVEY §8(d) ceilings of one SpMM (microseconds): compulsory HBM bytes,
+    the FP32 FMA pipe, and the L1 data path every gathered B row crosses
+    (4*bCols bytes per gcol at 128 B/clk/SM; profiles/r2_notes.md §1)."""
+    A, n = p.A, p.bcols
+    f = f_mhz * 1e6
+    bytes_comp = 8 * A.nnz + 4 * (A.m + 1) + 4 * A.k * n + 4 * A.m * n
+    return {"bytes_comp": bytes_comp,
+            "t_hbm_us": bytes_comp / (hbm_gbs * 1e9) * 1e6,
+            "t_fma_us": A.nnz * n / (n_sm * 128 * f) * 1e6,
+            "t_l1_us": 4.0 * n * G / (n_sm * 128 * f) * 1e6}
 
 
-def compare_baselines(torch, problems, dev, stream):
-    """Per-case hot-L2 times for escs, cuSPARSE (best of 4 algorithms),
-    cuBLAS fp32 and cuBLAS TF32 (context), same inputs, same protocol."""
+CASE_COLUMNS = ("case", "ufi", "t_escs_us", "t_escs_csr_us", "t_cusparse_us", "t_cublas_us",
+                "t_cublas_tf32_us", "gflops", "eff_GBps", "pct_hbm", "t_hbm_us", "t_fma_us",
+                "t_l1_us", "t_probe_us", "probe_frac", "attainable_frac", "binding")
+
+
+def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_csr=True):
+    """Per-case hot-L2 table (the paper's warm protocol): the timed
+    packed-record escs plan, the CSR-value walk of the same plan (escs_spmm),
+    cuSPARSE (best of 4 algorithms), cuBLAS fp32 / TF32 (dense A), the gather
+    probe of the plan, and the SURVEY §8(d) roofline bounds of the case."""
     import ctypes
     from paper_2506_15174_b200 import escs
     from paper_2506_15174_b200.build import BENCH_LIB
@@ -295,13 +346,20 @@ def compare_baselines(torch, problems, dev, stream):
     bl.bl_cublas_destroy.argtypes = [vp]
     cub = bl.bl_cublas_create()
     sp = stream.cuda_stream
-    rows = []
+    rows, best_algs = [], {}
     for p in problems:
         A, n = p.A, p.bcols
         d = dev[p.name]
-        st_escs = {}
-        t_escs = graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream,
-                            reps=20, stats=st_escs)
+        st = {}
+        t_escs = graph_time(torch, lambda: d["run"](stream), stream, reps=20, stats=st)
+        t_csr = (graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream)
+                 if with_csr else None)
+        t_probe = None
+        if d["probe"] is not None:
+            try:
+                t_probe = graph_time(torch, lambda: d["probe"](stream), stream)
+            except Exception:
+                t_probe = None
         rp = torch.from_numpy(A.rowptr).to(dev["_device"])
         ci = torch.from_numpy(A.colidx).to(dev["_device"])
         Cs = torch.empty_like(d["C"])
@@ -318,30 +376,111 @@ def compare_baselines(torch, problems, dev, stream):
             bl.bl_cusparse_destroy(h)
             if t and (best is None or t < best):
                 best, best_alg = t, alg
+        best_algs[p.name] = best_alg
         Ad = torch.from_numpy(A.dense()).to(dev["_device"])
         Cd = torch.empty_like(d["C"])
         t_cublas = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 0, sp), stream)
         t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
         del Ad
         inf = d["plan"].info
-        rows.append({"case": p.name, "escs_us": 1e3 * t_escs, "escs_us_min": 1e3 * st_escs["min"],
-                     "escs_us_p90": 1e3 * st_escs["p90"],
-                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")},
-                     "cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
-                     "cublas_us": 1e3 * t_cublas, "cublas_tf32_us": 1e3 * t_tf32,
-                     "gflops_escs": p.flops / (t_escs * 1e-3) / 1e9})
+        rb = roofline_bounds(p, inf["G"], n_sm, f_mhz, hbm_gbs)
+        t_us = 1e3 * t_escs
+        # the ceilings are lower bounds on the time (HBM bytes, FMA issue, L1
+        # data path); the probe (same walk, no FMAs) is reported beside them
+        # as a measurement, not a bound: it is compiled separately and is not
+        # guaranteed faster than the kernel
+        bounds = {"hbm": rb["t_hbm_us"], "fma": rb["t_fma_us"], "l1": rb["t_l1_us"]}
+        binding = max(bounds, key=bounds.get)
+        gbps = rb["bytes_comp"] / (t_us * 1e-6) / 1e9
+        rows.append({"case": p.name, "ufi": inf["h"], "t_escs_us": t_us,
+                     "t_escs_us_min": 1e3 * st["min"], "t_escs_us_p90": 1e3 * st["p90"],
+                     "t_escs_csr_us": None if t_csr is None else 1e3 * t_csr,
+                     "t_cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
+                     "t_cublas_us": 1e3 * t_cublas, "t_cublas_tf32_us": 1e3 * t_tf32,
+                     "gflops": p.flops / (t_us * 1e-6) / 1e9, "eff_GBps": gbps,
+                     "pct_hbm": 100.0 * gbps / hbm_gbs,
+                     "t_hbm_us": rb["t_hbm_us"], "t_fma_us": rb["t_fma_us"], "t_l1_us": rb["t_l1_us"],
+                     "t_probe_us": 1e3 * t_probe if t_probe else None,
+                     "probe_frac": (1e3 * t_probe / t_us) if t_probe else None,
+                     "attainable_frac": bounds[binding] / t_us, "binding": binding,
+                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")}})
     bl.bl_cublas_destroy(cub)
+    sel = lambda key: [r[key] for r in rows]
     out = {
-        "protocol": "hot L2, CUDA graph of R calls (R = clamp(2 ms / t, 10, 1000)) replayed 20x for escs, 11x for the baselines; median (paper P:675 warm cache); escs min and p90 per case",
-        "geomean_speedup_vs_cusparse": geomean([r["cusparse_us"] / r["escs_us"] for r in rows if r["cusparse_us"]]),
-        "geomean_speedup_vs_cublas": geomean([r["cublas_us"] / r["escs_us"] for r in rows]),
-        "geomean_speedup_vs_cublas_tf32": geomean([r["cublas_tf32_us"] / r["escs_us"] for r in rows]),
-        "pct_faster_than_cusparse": 100.0 * np.mean([r["cusparse_us"] is not None and r["escs_us"] < r["cusparse_us"] for r in rows]),
-        "pct_faster_than_cublas": 100.0 * np.mean([r["escs_us"] < r["cublas_us"] for r in rows]),
+        "protocol": ("hot L2, CUDA graph of R calls (R = clamp(2 ms / t, 10, 1000)) replayed 20x for escs, "
+                     "11x for the others; median (paper P:675 warm cache)"),
+        "geomean_speedup_vs_cusparse": geomean([r["t_cusparse_us"] / r["t_escs_us"] for r in rows if r["t_cusparse_us"]]),
+        "geomean_speedup_vs_cublas": geomean([r["t_cublas_us"] / r["t_escs_us"] for r in rows]),
+        "geomean_speedup_vs_cublas_tf32": geomean([r["t_cublas_tf32_us"] / r["t_escs_us"] for r in rows]),
+        "geomean_speedup_vs_csr_walk": (geomean([r["t_escs_csr_us"] / r["t_escs_us"] for r in rows])
+                                        if with_csr else None),
+        "pct_faster_than_cusparse": 100.0 * np.mean([r["t_cusparse_us"] is not None and r["t_escs_us"] < r["t_cusparse_us"] for r in rows]),
+        "pct_faster_than_cublas": 100.0 * np.mean([r["t_escs_us"] < r["t_cublas_us"] for r in rows]),
+        "median_attainable_frac": float(np.median(sel("attainable_frac"))),
+        "median_pct_hbm": float(np.median(sel("pct_hbm"))),
         "cases": len(rows),
         "paper_context": "A100: 1.84x vs cuBLAS, 2.27x vs cuSPARSE (abstract P:31); Table 1 geomeans 1.47x / 1.74x",
     }
-    return out, rows
+    return out, rows, best_algs
+
+
+def cusparse_multistream(torch, problems, dev, lanes, best_algs, steps, flush, sleep_cycles):
+    """cuSPARSE (each layer's best algorithm) on the same streams and LPT
+    partition as the multi-stream escs step: the like-for-like baseline of
+    that figure (L2 flushed per step, CUDA events on the forking stream)."""
+    import ctypes
+    from paper_2506_15174_b200 import shard
+    from paper_2506_15174_b200.build import BENCH_LIB
+    bl = ctypes.CDLL(BENCH_LIB)
+    vp = ctypes.c_void_p
+    bl.bl_cusparse_create.restype = vp
+    bl.bl_cusparse_create.argtypes = [ctypes.c_int] * 4 + [vp] * 5 + [ctypes.c_int, vp]
+    bl.bl_cusparse_run.argtypes = [vp, vp]
+    bl.bl_cusparse_destroy.argtypes = [vp]
+    groups = shard.partition_problems([p.flops for p in problems], len(lanes))
+    handles, keep = [], []
+    for gi, idx in enumerate(groups):
+        for i in idx:
+            p = problems[i]
+            d = dev[p.name]
+            rp = torch.from_numpy(p.A.rowptr).to(dev["_device"])
+            ci = torch.from_numpy(p.A.colidx).to(dev["_device"])
+            Cs = torch.empty_like(d["C"])
+            keep += [rp, ci, Cs]
+            h = bl.bl_cusparse_create(p.A.m, p.A.k, p.A.nnz, p.bcols, rp.data_ptr(), ci.data_ptr(),
+                                      d["vals"].data_ptr(), d["B"].data_ptr(), Cs.data_ptr(),
+                                      best_algs.get(p.name) or 0, lanes[gi].cuda_stream)
+            if not h:
+                return None
+            handles.append((h, lanes[gi]))
+    main = lanes[0]
+
+    def step():
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for s_ in lanes[1:]:
+            s_.wait_event(fork)
+        for h, s_ in handles:
+            bl.bl_cusparse_run(h, s_.cuda_stream)
+        for s_ in lanes[1:]:
+            j = torch.cuda.Event()
+            j.record(s_)
+            main.wait_event(j)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.zero_()
+        torch.cuda._sleep(sleep_cycles)
+        a.record(main)
+        step()
+        b.record(main)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    for h, _ in handles:
+        bl.bl_cusparse_destroy(h)
+    return sum(p.flops for p in problems) * steps / (ms * 1e-3) / 1e9
 
 
 def run_escs(args):
@@ -352,7 +491,7 @@ def run_escs(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # one process per GPU (LOCAL_RANK); ESCS_BENCH_BACKEND=gloo lets a 1-GPU box
-    # exercise the N > 1 control flow with several ranks sharing the device
+    # (or a CPU-only host with --cpu-dist-check) exercise the N > 1 control flow
     backend = os.environ.get("ESCS_BENCH_BACKEND", "nccl")
     local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
@@ -362,6 +501,10 @@ def run_escs(args):
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(backend)
+        nccl_v = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else "-"
+        print(f"[escs bench] rank {rank}/{world} local {local} device {torch.cuda.get_device_name(device)} "
+              f"backend {backend} nccl {nccl_v} pid {os.getpid()}", file=sys.stderr, flush=True)
+        dist.barrier()
 
     from paper_2506_15174_b200 import escs, shard, synth
 
@@ -378,108 +521,77 @@ def run_escs(args):
     else:
         mine = list(range(len(problems)))
         sharding = f"row-block x{world}"
+    packed = not args.csr
     dev = {"_device": device}
-    want_tp = bool(args.autotune and args.tp_plans and args.streams > 1 and len(mine) > 1)
     shard_problems = []
     plan_s = 0.0
-    plan_info = []
-    plan_info_tp = []
     for idx in mine:
         p = problems[idx]
         t0 = time.perf_counter()
-        tune = {"autotune": 1} if args.autotune else {}
+        prm = {"packed": 1 if packed else 0}
+        if args.ufi:
+            prm["ufi"] = args.ufi
+        if args.autotune and p.A.nnz <= 8_000_000:
+            prm["autotune"] = 1
         if mode == "problems":
             A = p.A
-            pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, **tune)
+            pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, **prm)
         else:
-            A, pl = shard.plan_shard(p.A, p.bcols, world, rank, **tune)
-        # throughput-objective plans (autotune = 2) for the multi-stream step:
-        # the latency-tuned plan of a layer alone tends to fill every SM, which
-        # starves the layers co-running on the other streams
-        pl_tp = None
-        if want_tp:
-            if mode == "problems":
-                pl_tp = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=2)
-            else:
-                pl_tp = shard.plan_shard(p.A, p.bcols, world, rank, autotune=2)[1]
+            A, pl = shard.plan_shard(p.A, p.bcols, world, rank, **prm)
         plan_s += time.perf_counter() - t0
         info = pl.info
-        plan_info.append(info)
-        plan_info_tp.append(pl_tp.info if pl_tp is not None else None)
-        d = {"plan": pl, "plan_tp": pl_tp or pl, "A": A,
-             "vals": torch.from_numpy(A.vals).to(device) if A.nnz else torch.zeros(1, device=device),
+        vals = torch.from_numpy(A.vals).to(device) if A.nnz else torch.zeros(1, device=device)
+        d = {"plan": pl, "A": A, "vals": vals,
              "B": torch.from_numpy(p.B).to(device),
              "C": torch.empty((A.m, p.bcols), dtype=torch.float32, device=device),
              "flops": 2 * A.nnz * p.bcols,
              "bytes": 8 * A.nnz + 4 * (A.m + 1) + 4 * A.k * p.bcols + 4 * A.m * p.bcols,
-             "gather_bytes": 4 * p.bcols * info["G"]}
+             "G": info["G"]}
+        if packed and info["variant"] == 1:
+            # the paper's data transformation, once per weight matrix
+            d["packed"] = escs.escs_pack(pl, vals)
+            d["run"] = (lambda d: lambda st, C=None: escs.escs_spmm_packed(
+                d["plan"], d["packed"], d["B"], d["C"] if C is None else C, st))(d)
+            sink = torch.empty(max(1, info["n_tiles"] * 32 * info["cta_warps"]), device=device)
+            d["probe"] = (lambda d, sink: lambda st: escs.escs_gather_probe_packed(
+                d["plan"], d["packed"], d["B"], sink, st))(d, sink)
+        else:
+            d["run"] = (lambda d: lambda st, C=None: escs.escs_spmm(
+                d["plan"], d["vals"], d["B"], d["C"] if C is None else C, st))(d)
+            sink = torch.empty(max(1, info["n_tiles"] * 32 * info["cta_warps"]), device=device)
+            d["probe"] = ((lambda d, sink: lambda st: escs.escs_gather_probe(d["plan"], d["B"], sink, st))(d, sink)
+                          if info["variant"] == 1 else None)
         dev[p.name] = d
         shard_problems.append((p, d))
+    torch.cuda.synchronize()
     flush = torch.empty(L2_FLUSH_BYTES // 4 if not args.hot_l2 else 4, dtype=torch.float32, device=device)
-    # all work on one non-default stream (graph capture needs a non-default stream)
-    stream = torch.cuda.Stream(device)
+    stream = torch.cuda.Stream(device)   # graph capture needs a non-default stream
     torch.cuda.set_stream(stream)
+    nprob = len(shard_problems)
 
-    # --streams S > 1: the independent problems of a suite run on S streams
-    # (LPT by flops), forked from and joined back into the timed stream, so
-    # small latency-bound layers overlap on the SMs (the suite analogue of the
-    # problem partition across ranks).  Each stream chains its launches with PDL.
-    nstreams = max(1, min(args.streams, len(shard_problems)))
+    def step(per_launch=None):
+        """One pass of the hot path: every layer's SpMM, one stream, in order."""
+        for i, (p, d) in enumerate(shard_problems):
+            if per_launch is not None:
+                per_launch[i][0].record(stream)
+            d["run"](stream)
+            if per_launch is not None:
+                per_launch[i][1].record(stream)
+
+    # multi-stream variant (reported beside value, with cuSPARSE on the same streams)
+    nstreams = max(1, min(args.streams, nprob))
     lanes = [stream] + [torch.cuda.Stream(device) for _ in range(nstreams - 1)]
     groups = shard.partition_problems([d["flops"] for _, d in shard_problems], nstreams)
     owner = {i: g for g, idx in enumerate(groups) for i in idx}
-    # multi-stream issue order: heaviest problems first (LPT list order), so
-    # the long layers start at once and the short ones fill in behind them
-    issue = (sorted(range(len(shard_problems)), key=lambda i: (-shard_problems[i][1]["flops"], i))
-             if args.issue_order == "lpt" else list(range(len(shard_problems))))
+    issue = sorted(range(nprob), key=lambda i: (-shard_problems[i][1]["flops"], i))
 
-    # --group: each stream's problems go through ONE escs_spmm_group call (one
-    # launch per kernel instance, <= 32 problems each, instead of one per problem)
-    grouped = None
-    group_launches = len(shard_problems)
-    if args.group:
-        grouped = [escs.Group([shard_problems[i][1]["plan_tp"] for i in idx],
-                              [shard_problems[i][1]["vals"] for i in idx],
-                              [shard_problems[i][1]["B"] for i in idx],
-                              [shard_problems[i][1]["C"] for i in idx]) for idx in groups]
-        group_launches = 0
-        for idx in groups:           # launches per call, as escs_spmm_group buckets them
-            keys = {}
-            for i in idx:
-                inf = shard_problems[i][1]["plan_tp"].info
-                if inf["h"] == 1 and inf["variant"] == 1:
-                    key = (inf["bcols"], inf["colf"], inf["ufk"], inf["cta_warps"])
-                    keys[key] = keys.get(key, 0) + 1
-                else:
-                    group_launches += 1
-            group_launches += sum(-(-c // 32) for c in keys.values())
-
-    def step(per_launch=None, serial=False):
-        if serial:      # every launch on the timed stream (the 1-stream figure)
-            for i, (p, d) in enumerate(shard_problems):
-                if per_launch is not None:
-                    per_launch[i][0].record(stream)
-                escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
-                if per_launch is not None:
-                    per_launch[i][1].record(stream)
-            return
-        if nstreams > 1:
-            fork = torch.cuda.Event()
-            fork.record(stream)
-            for s_ in lanes[1:]:
-                s_.wait_event(fork)
-        if grouped:
-            for g, st in zip(grouped, lanes):
-                g(stream=st)
-        else:
-            for i in issue:
-                p, d = shard_problems[i]
-                st = lanes[owner[i]]
-                if per_launch is not None:
-                    per_launch[i][0].record(st)
-                escs.escs_spmm(d["plan_tp"], d["vals"], d["B"], d["C"], st)
-                if per_launch is not None:
-                    per_launch[i][1].record(st)
+    def step_multi():
+        fork = torch.cuda.Event()
+        fork.record(stream)
+        for s_ in lanes[1:]:
+            s_.wait_event(fork)
+        for i in issue:
+            shard_problems[i][1]["run"](lanes[owner[i]])
         for s_ in lanes[1:]:
             j = torch.cuda.Event()
             j.record(s_)
@@ -490,16 +602,13 @@ def run_escs(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- warm-up
     for _ in range(args.warmup):
         step()
     barrier()
-
-    nprob = len(shard_problems)
     ev = lambda: torch.cuda.Event(enable_timing=True)
     sleep_cycles = int(2e6 + 4e4 * nprob)
 
-    # ---- timed: step events only (value)
+    # ---- timed: K steps, L2 flushed before each, step events only (value)
     starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
@@ -512,112 +621,101 @@ def run_escs(args):
             ends[s].record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
-        # ---- the same steps with every launch on one stream (reported beside value)
-        serial_ms = None
-        if nstreams > 1:
-            s0, s1 = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
-            for s in range(args.steps):
-                flush.zero_()
-                torch.cuda._sleep(sleep_cycles)
-                s0[s].record(stream)
-                step(serial=True)
-                s1[s].record(stream)
-            barrier()
-            serial_ms = sum(a.elapsed_time(b) for a, b in zip(s0, s1))
-        # ---- timed again with per-launch events (kernel durations for the roofline;
-        # one stream, so each duration is the kernel alone)
+        # ---- the same steps with per-launch events (each kernel's duration,
+        # the dominant kernel's roofline; one stream, so each kernel is alone)
         pl_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
         for s in range(args.steps):
             flush.zero_()
             torch.cuda._sleep(sleep_cycles)
-            step(pl_ev[s], serial=True)   # kernels alone, like the probe below
+            step(pl_ev[s])
         barrier()
-    # ---- gather probe: same walk and B-row loads, no values/FMAs (t_probe)
+        # ---- multi-stream step (independent layers overlapped on S streams)
+        multi_ms = None
+        if nstreams > 1:
+            for _ in range(args.warmup):
+                step_multi()
+            barrier()
+            m0, m1 = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+            for s in range(args.steps):
+                flush.zero_()
+                torch.cuda._sleep(sleep_cycles)
+                m0[s].record(stream)
+                step_multi()
+                m1[s].record(stream)
+            barrier()
+            multi_ms = sum(a.elapsed_time(b) for a, b in zip(m0, m1))
+    # ---- gather probe per launch (t_probe), L2 flushed per step
     probe_ms = None
-    if all(d["plan"].info["variant"] == 1 for _, d in shard_problems):
-        sinks = [torch.empty(d["plan"].info["n_tiles"] * 32 * d["plan"].info["cta_warps"],
-                             device=device) for _, d in shard_problems]
+    if all(d["probe"] is not None for _, d in shard_problems):
         pr_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
         for s_ in range(args.steps):
             flush.zero_()
             torch.cuda._sleep(sleep_cycles)
             for i, (p, d) in enumerate(shard_problems):
                 pr_ev[s_][i][0].record(stream)
-                escs.escs_gather_probe(d["plan"], d["B"], sinks[i], stream)
+                d["probe"](stream)
                 pr_ev[s_][i][1].record(stream)
         barrier()
-        probe_ms = float(sum(a.elapsed_time(b) for row in pr_ev for a, b in row))
+        probe_ms = np.array([[a.elapsed_time(b) for a, b in pr_ev[s]] for s in range(args.steps)])
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
     total_ms = sum(step_ms)
     kern_ms = np.array([[a.elapsed_time(b) for a, b in pl_ev[s]] for s in range(args.steps)])
-    kern_ms_sum = float(kern_ms.sum())
 
-    # ---- e2e: host buffers through the public API, copies inside the timed region.
-    # The step's inputs (every layer's values and B) sit in one pinned host
-    # buffer and its outputs land in one pinned host buffer; the step is cut
-    # into --e2e-chunks chunks of layers pipelined over three streams (H2D of
-    # chunk j+1 overlaps the SpMMs of chunk j; D2H of chunk j follows its
-    # SpMMs on its own stream, overlapping later H2D and SpMMs).
-    sizes_in = [(d["A"].nnz, p.B.size) for p, d in shard_problems]
-    off_in, tot_in = [], 0
-    for nv, nb in sizes_in:
-        off_in.append(tot_in)
-        tot_in += (max(nv, 1) + 3) // 4 * 4 + nb   # 16-byte aligned B views
-    off_out, tot_out = [], 0
-    for _, d in shard_problems:
-        off_out.append(tot_out)
-        tot_out += d["C"].numel()
-    vpad = [(max(nv, 1) + 3) // 4 * 4 for nv, _ in sizes_in]
+    # ---- e2e through the public API with host buffers: every step copies its
+    # inputs (each layer's B, the activations) from pinned host memory and
+    # reads every C back; the sparse weights are resident in their transformed
+    # form (escs_pack once, the paper's TA reused across inference).
+    # Chunks of layers are pipelined over three streams (H2D of chunk j+1
+    # overlaps the SpMMs of chunk j; D2H of chunk j on its own stream).
+    sizes_in = [p.B.size for p, _ in shard_problems]
+    off_in = np.concatenate([[0], np.cumsum([(x + 3) // 4 * 4 for x in sizes_in])]).astype(np.int64)
+    off_out = np.concatenate([[0], np.cumsum([d["C"].numel() for _, d in shard_problems])]).astype(np.int64)
+    tot_in, tot_out = int(off_in[-1]), int(off_out[-1])
     h_in = torch.zeros(tot_in, dtype=torch.float32).pin_memory()
     h_out = torch.empty(tot_out, dtype=torch.float32).pin_memory()
     for i, (p, d) in enumerate(shard_problems):
-        nv, nb = sizes_in[i]
-        if nv:
-            h_in[off_in[i]:off_in[i] + nv] = torch.from_numpy(d["A"].vals)
-        h_in[off_in[i] + vpad[i]:off_in[i] + vpad[i] + nb] = torch.from_numpy(p.B.ravel())
+        h_in[int(off_in[i]):int(off_in[i]) + p.B.size] = torch.from_numpy(p.B.ravel())
     d_in = torch.empty(tot_in, dtype=torch.float32, device=device)
     d_out = torch.empty(tot_out, dtype=torch.float32, device=device)
+    copy_s, out_s = torch.cuda.Stream(device), torch.cuda.Stream(device)
     nchunk = min(args.e2e_chunks, nprob)
-    # equal layer counts per chunk (measured: 880 GFLOP/s vs 785 with chunks
-    # balanced by bytes -- a small first chunk starts the pipeline sooner)
     bounds = [(c * nprob) // nchunk for c in range(nchunk + 1)]
-    copy_s = torch.cuda.Stream(device)
-    out_s = torch.cuda.Stream(device)
-    h2d = 4 * tot_in
-    d2h = 4 * tot_out
+    h2d, d2h = 4 * tot_in, 4 * tot_out
+    views = []
+    for i, (p, d) in enumerate(shard_problems):
+        Bv = d_in[int(off_in[i]):int(off_in[i]) + p.B.size]
+        Cv = d_out[int(off_out[i]):int(off_out[i + 1])]
+        views.append((Bv, Cv))
+
+    def run_with(d, Bv, Cv, st):
+        if "packed" in d:
+            escs.escs_spmm_packed(d["plan"], d["packed"], Bv, Cv, st)
+        else:
+            escs.escs_spmm(d["plan"], d["vals"], Bv, Cv, st)
 
     def e2e_step():
         evs = []
-        for c in range(nchunk):            # H2D of every chunk on the copy stream
-            a, b = bounds[c], bounds[c + 1]
-            lo, hi = off_in[a], (off_in[b] if b < nprob else tot_in)
+        for c in range(nchunk):
+            lo, hi = int(off_in[bounds[c]]), int(off_in[bounds[c + 1]])
             copy_s.wait_stream(stream)
             with torch.cuda.stream(copy_s):
                 d_in[lo:hi].copy_(h_in[lo:hi], non_blocking=True)
             e = torch.cuda.Event()
             e.record(copy_s)
             evs.append(e)
-        for c in range(nchunk):            # SpMMs on the main stream, then D2H of the chunk
+        for c in range(nchunk):
             stream.wait_event(evs[c])
-            a, b = bounds[c], bounds[c + 1]
-            for i in range(a, b):
-                p, d = shard_problems[i]
-                nv, nb = sizes_in[i]
-                v = d_in[off_in[i]:off_in[i] + vpad[i]]
-                Bv = d_in[off_in[i] + vpad[i]:off_in[i] + vpad[i] + nb]
-                Cv = d_out[off_out[i]:off_out[i] + d["C"].numel()]
-                escs.escs_spmm(d["plan"], v, Bv, Cv, stream)
-            lo, hi = off_out[a], (off_out[b] if b < nprob else tot_out)
+            for i in range(bounds[c], bounds[c + 1]):
+                run_with(shard_problems[i][1], views[i][0], views[i][1], stream)
+            lo, hi = int(off_out[bounds[c]]), int(off_out[bounds[c + 1]])
             out_s.wait_stream(stream)
-            with torch.cuda.stream(out_s):         # D2H on its own engine/stream
+            with torch.cuda.stream(out_s):
                 h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
         stream.wait_stream(out_s)
 
     if nprob == 1 and args.e2e_chunks > 1 and shard_problems[0][1]["A"].m >= 8 * args.e2e_chunks:
-        # one large problem: pipeline by row blocks (one escs plan per block,
-        # built once, outside the timed region).  H2D of B first, then each
-        # block's values (contiguous in CSR order) while earlier blocks compute;
-        # each block's C rows go back as soon as they are done.
+        # one large problem: B in, then row blocks (one plan per block, built
+        # and packed once) computed while earlier blocks' C rows go back
         p0, d0 = shard_problems[0]
         A0, n0 = d0["A"], p0.bcols
         E = args.e2e_chunks
@@ -625,34 +723,26 @@ def run_escs(args):
         for r in range(E):
             r0, r1 = synth.shard_bounds(A0.m, E, r)
             S = synth.row_block(A0, r0, r1)
-            tune = {"autotune": 1} if args.autotune and S.nnz <= 8_000_000 else {}
-            pl = escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, n0, **tune)
-            blocks.append((pl, int(A0.rowptr[r0]), S.nnz, r0, r1))
-        bpad = (p0.B.size + 3) // 4 * 4
-        h_in = torch.empty(bpad + max(A0.nnz, 1), dtype=torch.float32).pin_memory()
-        h_in[:p0.B.size] = torch.from_numpy(p0.B.ravel())
-        if A0.nnz:
-            h_in[bpad:bpad + A0.nnz] = torch.from_numpy(A0.vals)
-        h_out = torch.empty(A0.m * n0, dtype=torch.float32).pin_memory()
-        d_in = torch.empty_like(h_in, device=device)
-        d_out = torch.empty(A0.m * n0, dtype=torch.float32, device=device)
-        h2d, d2h = 4 * (p0.B.size + A0.nnz), 4 * A0.m * n0
+            prm = {"packed": 1 if packed else 0}
+            if args.autotune and S.nnz <= 8_000_000:
+                prm["autotune"] = 1
+            pl = escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, n0, **prm)
+            sv = torch.from_numpy(S.vals).to(device) if S.nnz else torch.zeros(1, device=device)
+            bd = {"plan": pl, "vals": sv}
+            if packed and pl.info["variant"] == 1:
+                bd["packed"] = escs.escs_pack(pl, sv)
+            blocks.append((bd, r0, r1))
         Bv = d_in[:p0.B.size]
 
         def e2e_step():
-            evs = []
             copy_s.wait_stream(stream)
             with torch.cuda.stream(copy_s):
                 d_in[:p0.B.size].copy_(h_in[:p0.B.size], non_blocking=True)
-                for pl, v0, nv, r0, r1 in blocks:
-                    d_in[bpad + v0:bpad + v0 + nv].copy_(h_in[bpad + v0:bpad + v0 + nv], non_blocking=True)
-                    e = torch.cuda.Event()
-                    e.record(copy_s)
-                    evs.append(e)
-            for (pl, v0, nv, r0, r1), e in zip(blocks, evs):
-                stream.wait_event(e)
-                vv = d_in[bpad + v0:bpad + v0 + max(nv, 1)]
-                escs.escs_spmm(pl, vv, Bv, d_out[r0 * n0:r1 * n0], stream)
+            e = torch.cuda.Event()
+            e.record(copy_s)
+            stream.wait_event(e)
+            for bd, r0, r1 in blocks:
+                run_with(bd, Bv, d_out[r0 * n0:r1 * n0], stream)
                 out_s.wait_stream(stream)
                 with torch.cuda.stream(out_s):
                     h_out[r0 * n0:r1 * n0].copy_(d_out[r0 * n0:r1 * n0], non_blocking=True)
@@ -670,15 +760,14 @@ def run_escs(args):
         ee[s].record(stream)
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in zip(es, ee))
-    # the copies alone (same buffers, same chunking): the PCIe floor of e2e
     ca, cb = ev(), ev()
     ca.record(stream)
     for _ in range(args.steps):
+        copy_s.wait_stream(stream)
+        out_s.wait_stream(stream)
         with torch.cuda.stream(copy_s):
-            copy_s.wait_stream(stream)
             d_in.copy_(h_in, non_blocking=True)
         with torch.cuda.stream(out_s):
-            out_s.wait_stream(stream)
             h_out.copy_(d_out, non_blocking=True)
         stream.wait_stream(copy_s)
         stream.wait_stream(out_s)
@@ -697,16 +786,15 @@ def run_escs(args):
         gb.record(stream)
         barrier()
         allgather_ms = shard.max_over_ranks([ga.elapsed_time(gb)], device)[0]
-    # ---- SpMM fused with the all-gather (NEXT f1): escs_spmm_scatter stores
-    # each C row into every rank's symmetric-memory C (NVLink P2P / NVLS
-    # multicast); timed per step against SpMM + NCCL all-gather
     fused = None
     if world > 1 and args.allgather and mode == "rows" and backend == "nccl":
         try:
             fgs = [shard.FusedGather(p.A.m, p.bcols) for p, _ in shard_problems]
+
             def fused_step():
                 for fg, (p, d) in zip(fgs, shard_problems):
                     fg.run(d["plan"], d["vals"], d["B"], stream)
+
             def split_step():
                 for p, d in shard_problems:
                     escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream)
@@ -729,8 +817,7 @@ def run_escs(args):
     # ---- reduce over ranks: flops SUM, times MAX
     my_flops = sum(d["flops"] for _, d in shard_problems)
     my_bytes = sum(d["bytes"] for _, d in shard_problems)
-    total_ms, e2e_ms, kern_ms_sum, serial_ms = shard.max_over_ranks(
-        [total_ms, e2e_ms, kern_ms_sum, serial_ms or 0.0], device)
+    total_ms, e2e_ms, multi_max = shard.max_over_ranks([total_ms, e2e_ms, multi_ms or 0.0], device)
     flops_all, bytes_all = shard.sum_over_ranks([my_flops, my_bytes], device)
 
     result = None
@@ -738,103 +825,113 @@ def run_escs(args):
         hbm, peak_src, mp = peaks()
         K = args.steps
         value = flops_all * K / (total_ms * 1e-3) / 1e9
-        # roofline of the (only) kernel: compulsory bytes per launch / launch duration
-        achieved = my_bytes * K / (kern_ms.sum() * 1e-3) / 1e9
-        gather = sum(d["gather_bytes"] for _, d in shard_problems) * K / (total_ms * 1e-3) / 1e9
-        per_prob = kern_ms.mean(axis=0)
-        dom = int(np.argmax(per_prob))
-        clocks = clk.summary()
-        traffic, traffic_src = committed_traffic(args.workload) if world == 1 else (None, None)
         n_sm = torch.cuda.get_device_properties(device).multi_processor_count
-        gather_derived = n_sm * 64.0 * float(mp.get("sm_max_mhz", 1965.0)) * 1e6 / 1e9
-        try:
-            gather_peak, gather_src = gather_ceiling(torch, device, stream, n_sm), (
-                "measured in this run: bl_gather_peak (libescs_bench.so) gathers pseudo-random 512-byte "
-                "rows of a 64 MiB L2-resident B, no index loads / values / FMAs, best of 6 lane maps")
-        except (OSError, AssertionError):
-            gather_peak, gather_src = gather_derived, "derived: SMs x 64 B/clk x max SM clock"
-        step_bytes_per_s = my_bytes * K / (total_ms * 1e-3) / 1e9
+        f_mhz = float(mp.get("sm_max_mhz", 1965.0))
+        per_prob = kern_ms.mean(axis=0)                # ms per launch, L2 flushed per step
+        dom = int(np.argmax(per_prob))
+        pd, dd = shard_problems[dom]
+        rb = roofline_bounds(pd, dd["G"], n_sm, f_mhz, hbm)
+        t_dom_us = 1e3 * float(per_prob[dom])
+        dom_gbs = rb["bytes_comp"] / (t_dom_us * 1e-6) / 1e9
+        clocks = clk.summary()
+        traffic, traffic_src = committed_traffic(args.workload, pd.name) if world == 1 else (None, None)
+        infos = [d["plan"].info for _, d in shard_problems]
+        ufi_mix = {}
+        for inf in infos:
+            ufi_mix[str(inf["h"])] = ufi_mix.get(str(inf["h"]), 0) + 1
+        step_gbs = bytes_all * K / (total_ms * 1e-3) / 1e9
+        dinf = infos[dom]
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "problems": len(problems), "sharding": sharding,
-                       "streams": nstreams,
-                       "grouped": bool(args.group),
+            "scaling": "weak" if (world > 1 and mode == "problems") else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "problems": len(problems), "sharding": sharding, "streams": 1,
                        "l2": ("flushed before every step (256 MiB write); each problem touched once per step"
                               if not args.hot_l2 else "NOT flushed (--hot-l2 diagnostic, not a bench value)"),
-                       "plans": (("autotuned at plan time (escs_params.autotune: timed T / tile width / UFk candidates); "
-                                  + ("the multi-stream step (value) runs throughput-objective plans (autotune=2: candidates "
-                                     "timed as 8 concurrent launch chains on 8 streams), serial / per-launch / per-case figures "
-                                     "the latency-objective plans (autotune=1)" if want_tp else "latency objective (autotune=1)"))
+                       "path": ("escs_spmm_packed: the packed record walk on escs_pack's stream (the paper's data "
+                                "transformation, done once per weight matrix at setup, P:575-578)"
+                                if packed else "escs_spmm: the CSR-value walk (--csr)"),
+                       "plans": ("autotuned at plan time for this walk (escs_params.autotune=1, latency objective; "
+                                 + ("UFi searched 1..4" if packed and not args.ufi else f"UFi fixed {args.ufi or 1}")
+                                 + "; problems above 8M nonzeros use the parameter table)"
                                  if args.autotune else "parameter table (escs_plan defaults)"),
-                       "plan": {k: plan_info[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")},
-                       "plan_throughput": ({k: plan_info_tp[dom][k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant")}
-                                           if plan_info_tp[dom] is not None else None)},
-            "roofline": {"bound": "hbm", "achieved": step_bytes_per_s, "peak": hbm, "unit": "GB/s",
-                         "frac": step_bytes_per_s / hbm, "traffic": traffic,
-                         "achieved_how": ("algorithmic bytes of the step / timed step (CUDA events on the "
-                                          "launching streams; the timed region holds only escs_spmm launches, "
-                                          "back to back with PDL on each of config.streams streams)"),
-                         "achieved_per_launch_bracketed": achieved,
-                         "traffic_source": traffic_src,
-                         "algorithmic_bytes_per_launch": my_bytes / nprob,
-                         "peak_source": peak_src,
-                         "algorithmic_bytes": "8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols per launch (CSR A, B, C once; SURVEY 8(d))",
-                         "kernel": "escs_spmm (esc_spmm_kernel), all launches of the step",
-                         "kernel_ms_per_step": float(kern_ms.sum() / K),
-                         "kernel_ms_how": "sum of per-launch CUDA-event durations, launches on one stream (each kernel alone)",
-                         "gather_GBps": gather,
-                         "gather_bytes": "4*bCols per gcol (one B row per (panel,column) pair)",
-                         "gather_roofline": {
-                             "achieved": gather, "unit": "GB/s",
-                             "peak": gather_peak, "frac": gather / gather_peak,
-                             "peak_source": gather_src,
-                             "derived_64B_per_clk": gather_derived},
-                         "attainable": None if probe_ms is None else {
-                             "probe_ms_per_step": probe_ms / K,
-                             "frac": probe_ms / float(kern_ms.sum()),
-                             "what": "t_probe / t_kernel: escs_gather_probe runs the same item walk and B-row gathers without values or FMAs (measured gather ceiling of this plan)"}},
-            "gpu_launches": group_launches * K,   # this rank's kernel launches in the timed region
+                       "ufi_forced": args.ufi or None,
+                       "ufi_mix": ufi_mix,
+                       "pdl": bool(dinf["pdl"]),
+                       "plan": {k: dinf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant", "n_tiles", "n_heavy", "pdl", "packed")}},
+            "roofline": {
+                "bound": "hbm", "achieved": dom_gbs, "peak": hbm, "unit": "GB/s", "frac": dom_gbs / hbm,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": f"{'esc_rec_kernel' if dinf['packed'] else 'esc_spmm_kernel'} on the dominant layer {pd.name}",
+                "achieved_how": ("compulsory bytes (8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols, SURVEY 8(d)) of the "
+                                 "dominant layer / its mean launch duration (CUDA events around each launch on the "
+                                 "launching stream, L2 flushed before every step, launches in order on one stream)"),
+                "kernel_us": t_dom_us, "algorithmic_bytes_per_launch": rb["bytes_comp"],
+                "peak_source": peak_src,
+                "l1_gather_ceiling": {"t_l1_us": rb["t_l1_us"], "frac": rb["t_l1_us"] / t_dom_us,
+                                      "what": "4*bCols bytes per gcol (plan G) through 128 B/clk/SM at the max SM clock "
+                                              "(profiles/r2_notes.md 1): the ceiling that binds, not HBM"},
+                "t_fma_us": rb["t_fma_us"], "t_hbm_us": rb["t_hbm_us"],
+                "t_probe_us": None if probe_ms is None else 1e3 * float(probe_ms.mean(axis=0)[dom]),
+                "step_aggregate": {"achieved": step_gbs, "frac": step_gbs / hbm,
+                                   "what": "compulsory bytes of the whole step / the timed step (1 stream)"},
+                "attainable": None if probe_ms is None else {
+                    "probe_ms_per_step": float(probe_ms.sum() / K),
+                    "frac": float(probe_ms.sum() / kern_ms.sum()),
+                    "what": "t_probe / t_kernel summed over the step's launches (escs_gather_probe[_packed]: same walk and "
+                            "B-row gathers, no FMAs)"}},
+            "gpu_launches": nprob * K,
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "inputs": "every layer's B (activations) H2D and every C D2H per step; the transformed sparse "
+                              "weights are resident (built once)",
                     "copies_only_ms_per_step": copy_ms,
                     "copy_floor": (f"{(h2d + d2h) / (copy_ms * 1e-3) / 1e9:.1f} GB/s host<->device "
-                                   f"(H2D and D2H concurrent); e2e is {e2e_ms / K / copy_ms:.2f}x "
-                                   "the copies alone")},
+                                   f"(H2D and D2H concurrent); e2e is {e2e_ms / K / max(copy_ms, 1e-9):.2f}x the copies alone")},
             "plan_seconds": plan_s,
         }
-        if nstreams > 1:
-            result["serial"] = {"value": flops_all * K / (serial_ms * 1e-3) / 1e9, "unit": UNIT,
-                                "ms_per_step": serial_ms / K,
-                                "what": "same steps, every escs_spmm on one stream (PDL chain)"}
+        if multi_ms:
+            result["multistream"] = {"streams": nstreams, "value": flops_all * K / (multi_max * 1e-3) / 1e9,
+                                     "unit": UNIT, "ms_per_step": multi_max / K,
+                                     "what": "the same plans with the independent layers LPT-partitioned over "
+                                             "several streams (context; value is the one-stream step)"}
         if allgather_ms is not None:
             result["allgather_ms_per_step"] = allgather_ms
         if fused is not None:
             result["fused_allgather"] = fused
         if world == 1 and not args.no_cpu:
-            v, reps, secs, thr = oracle_time(problems, budget_s=args.cpu_budget)
-            result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
-                                      "sample": f"whole workload x{reps} ({secs:.1f} s), fp64 C oracle"}
-            # one-time planning costs (the paper excludes its dataTransformer from
-            # SpMM time): escs_plan (h-way merge, threaded, incl. autotuning)
-            # vs the oracle's dense-scan partitioner (O(m*k) per problem)
+            v, reps, secs, thr, sample = oracle_time(problems, budget_s=args.cpu_budget)
+            result["cpu_baseline"] = dict({"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+                                           "sample": f"{sample} ({secs:.1f} s), fp64 C oracle"},
+                                          **cpu_info(thr))
+            result["cpu_baseline"]["c1_single_thread"] = oracle_c1_single_thread()
             if sum(p.A.m * p.A.k for p in problems) <= 2e9:
                 import oracle
                 t0 = time.perf_counter()
                 for p, d in shard_problems:
                     inf = d["plan"].info
                     oracle.partition(p.A.m, p.A.k, p.A.rowptr, p.A.colidx, inf["h"], inf["T"], p.bcols)
-                result["planning"] = {"escs_plan_s": plan_s,
-                                      "oracle_partition_s": time.perf_counter() - t0,
-                                      "what": "one-time host planning for the whole workload (not in value)"}
+                result["planning"] = {"escs_plan_s": plan_s, "oracle_partition_s": time.perf_counter() - t0,
+                                      "what": "one-time host planning for the whole workload incl. autotuning "
+                                              "(not in value)"}
         if world == 1 and not args.no_compare:
-            summ, rows = compare_baselines(torch, problems, dev, stream)
+            summ, rows, best_algs = compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm,
+                                                      with_csr=packed)
             result["baselines"] = summ
+            result["cases_columns"] = list(CASE_COLUMNS)
+            result["cases"] = [[r[c] if not isinstance(r[c], float) else round(r[c], 4) for c in CASE_COLUMNS]
+                               for r in rows]
             if args.cases_out:
                 with open(args.cases_out, "w") as f:
                     json.dump(rows, f, indent=1)
+            if multi_ms and nstreams > 1:
+                cs = cusparse_multistream(torch, [p for p, _ in shard_problems], dev, lanes, best_algs,
+                                          args.steps, flush, sleep_cycles)
+                if cs:
+                    result["multistream"]["cusparse_value"] = cs
+                    result["multistream"]["vs_cusparse"] = result["multistream"]["value"] / cs
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -855,15 +952,13 @@ def main(argv=None):
     ap.add_argument("--hot-l2", action="store_true",
                     help="diagnostic only: skip the L2 flush between steps (not a bench value)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--group", type=int, default=0,
-                    help="1: each stream's problems in one escs_spmm_group call (grouped launches)")
-    ap.add_argument("--issue-order", default="lpt", choices=("lpt", "index"),
-                    help="multi-stream step: launch problems heaviest-first (lpt) or in suite order")
     ap.add_argument("--streams", type=int, default=16,
-                    help="suite: run the independent problems on this many streams (LPT by flops)")
+                    help="also time the suite with its layers on this many streams (context figure)")
     ap.add_argument("--cases-out", default=None)
-    ap.add_argument("--no-tp-plans", dest="tp_plans", action="store_false",
-                    help="run the multi-stream step on the latency-tuned plans too (no autotune=2 plans)")
+    ap.add_argument("--csr", action="store_true",
+                    help="time escs_spmm on the CSR values (the CSR-value walk) instead of the packed record walk")
+    ap.add_argument("--ufi", type=int, default=0,
+                    help="force UFi for every plan (e.g. 4: the enumerated path); 0 = tuned")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table only (default: plan-time autotuning)")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],

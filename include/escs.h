@@ -136,8 +136,11 @@ int escs_spmm_group(int32_t n, const escs_plan_t *plans, const float *const *val
  *   UFi = 2, 3   int32 {col | mask << 27, w_0 .. w_{h-1}, 0 ..}    4 words
  *   UFi = 4      int32 {col | mask << 27, w_0, w_1, w_2, w_3, 0, 0, 0}  8 words
  * (w_r = the value of A(panel*h + r, col), 0.0 for rows outside the pattern;
- * values are copied bit for bit).  One kernel launch on `stream`,
- * enqueue-only.
+ * values are copied bit for bit).  One kernel launch on `stream`; SYNCHRONOUS
+ * (returns after the stream has finished it): like the plan, the record
+ * stream is then immutable input -- escs_spmm_packed may read it before the
+ * previous kernel in its stream has finished (programmatic dependent
+ * launch); rewrite it only through escs_pack.
  *   vals    DEVICE float[nnz], CSR order.
  *   packed  DEVICE buffer of escs_plan_stats.packed_words 32-bit words,
  *           16-byte aligned, caller-owned output; must not alias vals.

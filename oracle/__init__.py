@@ -29,23 +29,57 @@ PLAN_HEADER_FIELDS = ("version", "m", "k", "nnz", "bCols", "h", "T",
                       "nP", "NG", "G", "n_items")
 
 
+_FLAGS = ["-O3", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with plain gcc (-O2, OpenMP over rows only)."""
+    """Compile the oracle with plain gcc (-O3, no FMA contraction, OpenMP over
+    rows only; portable: this library travels to other hosts)."""
     if _LIB_OVERRIDE:
         return _LIB
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared",
-                               "-std=c11", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc"] + _FLAGS + ["-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
+
+
+def use_native() -> str:
+    """bench.py's cpu_baseline: the same source built -O3 -march=native on the
+    host that runs it (the oracle timed as a tuned C build) and
+    loaded in place of the portable library for this process.  Returns the
+    library path.  The arithmetic is unchanged: fp64 sums in CSR order, no FMA
+    contraction (and every fp32 x fp32 product is exact in fp64 anyway)."""
+    global _lib
+    path = os.path.join(_HERE, f"liboracle_native_{os.uname().nodename}.so")
+    if not os.path.exists(path) or os.path.getmtime(path) < os.path.getmtime(_SRC):
+        tmp = path + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc"] + _FLAGS + ["-march=native", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, path)
+    with _lock:
+        _lib = None
+    os.environ["ESCS_ORACLE_LIB"] = path
+    globals()["_LIB"] = path
+    return path
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _load():
     global _lib
     with _lock:
         if _lib is None:
-            build()
+            if _LIB == os.path.join(_HERE, "liboracle.so"):
+                build()
             lib = ctypes.CDLL(_LIB)
             P = ctypes.c_void_p
             i64, i32 = ctypes.c_int64, ctypes.c_int32

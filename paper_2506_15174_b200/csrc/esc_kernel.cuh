@@ -493,7 +493,8 @@ __device__ __forceinline__ void ld_rec(int (&r)[RW], const int* q) {
 // a 128-byte line holds the next 4-16 records of the (sub-)warp.
 template <int H, class Map, int U, bool TAIL, bool PROBE, class PP>
 __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, int end, int sub,
-                                          int lj, float (&acc)[H][Map::F], unsigned long long pol_b) {
+                                          int lj, int lane, float (&acc)[H][Map::F],
+                                          unsigned long long pol_b) {
     constexpr int F = Map::F, S = Map::S, RW = RecFmt<H>::W, N = Map::L * Map::F;
     int r[U][RW];
     float b[U][F];
@@ -502,6 +503,15 @@ __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, in
         const int idx = i + u * S + sub;
         ld_rec<RW>(r[u], rec + (size_t)(TAIL ? min(idx, end - 1) : idx) * RW);
         if (TAIL && H > 1 && idx >= end) r[u][0] &= kColMask;   // no pattern rows
+    }
+    if constexpr (!TAIL) {
+        // the record lines two batches ahead into L1: with a cold L2 (the
+        // bench flushes it per step) a record line is a DRAM round trip that
+        // would otherwise sit between two batches' B gathers
+        constexpr int kLines = (U * S * RW * 4 + 127) / 128;
+        const int ahead = i + 2 * U * S;
+        if (lane < kLines && ahead + lane * (128 / (RW * 4)) < end)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (size_t)ahead * RW + lane * 32));
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -534,11 +544,22 @@ __device__ __forceinline__ void walk_rec(const PP& p, int beg, int end, float (&
     const int sub = lane / Map::L, lj = lane % Map::L;
     const int* rec = reinterpret_cast<const int*>(p.vals);
     const unsigned long long pol_b = policy_last();
-    grid_dep_wait();   // records and B are caller data
+    // The record stream is immutable once escs_pack has returned (escs_pack
+    // synchronises its stream, include/escs.h), so -- like the plan -- its
+    // first lines may be fetched before the programmatic-dependent-launch wait,
+    // overlapping the previous kernel's tail; B is caller data written by that
+    // kernel and is read only after the wait.
+    {
+        constexpr int kLines = (2 * US * RecFmt<H>::W * 4 + 127) / 128;   // the first two batches
+        if (lane < kLines && beg + lane * (128 / (RecFmt<H>::W * 4)) < end)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (size_t)beg * RecFmt<H>::W + lane * 32));
+    }
+    grid_dep_wait();
     int i = beg;
 #pragma unroll 1
-    for (; i + US <= end; i += US) rec_batch<H, Map, U, false, PROBE, PP>(p, rec, i, end, sub, lj, acc, pol_b);
-    if (i < end) rec_batch<H, Map, U, true, PROBE, PP>(p, rec, i, end, sub, lj, acc, pol_b);
+    for (; i + US <= end; i += US)
+        rec_batch<H, Map, U, false, PROBE, PP>(p, rec, i, end, sub, lj, lane, acc, pol_b);
+    if (i < end) rec_batch<H, Map, U, true, PROBE, PP>(p, rec, i, end, sub, lj, lane, acc, pol_b);
 }
 
 // Row r of a panel tile is written by sub-warp r % S (after the sub-warp

@@ -192,23 +192,38 @@ def test_unaligned_pointers_take_scalar_path(torch_cuda):
     check_exact(A, B, bufC[1:].cpu().numpy().reshape(A.m, 64))
 
 
+def run_path(torch, A, B, packed, **params):
+    """One SpMM through the C ABI, CSR-value walk or packed record walk (the
+    path bench.py times: escs_pack once, escs_spmm_packed)."""
+    from paper_2506_15174_b200 import escs
+    n = B.shape[1]
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, packed=1 if packed else 0, **params)
+    dv = torch.from_numpy(A.vals).cuda() if A.nnz else torch.zeros(1, device="cuda")
+    dB = torch.from_numpy(np.ascontiguousarray(B)).cuda()
+    dC = torch.full((A.m, n), float("nan"), device="cuda")
+    if packed:
+        escs.escs_spmm_packed(pl, escs.escs_pack(pl, dv), dB, dC)
+    else:
+        escs.escs_spmm(pl, dv, dB, dC)
+    torch.cuda.synchronize()
+    return dC.cpu().numpy(), pl
+
+
+@pytest.mark.parametrize("packed", [0, 1])
 @pytest.mark.parametrize("autotune", [0, 1])
-def test_c4_full_size(torch_cuda, autotune):
-    """C4 at full size, default plan and the autotuned plan bench.py times
-    (heavy panels, 16-column lane tiles): sampled rows incl. every dense row."""
+def test_c4_full_size(torch_cuda, autotune, packed):
+    """C4 at full size, every row: the default plan and the autotuned plan
+    (bench.py --workload c4 times the autotuned packed one; heavy panels,
+    wide lane tiles), G2/G3 on the real values and exact on the dyadic twin."""
     p = synth.config("c4")
     prm = {"autotune": 1} if autotune else {}
-    C, pl = run_escs(torch_cuda, p.A, p.B, **prm)
+    C, pl = run_path(torch_cuda, p.A, p.B, packed, **prm)
     info = pl.info
-    rng = np.random.default_rng(0)
-    lens = np.diff(p.A.rowptr)
-    rows = np.unique(np.concatenate([rng.choice(p.A.m, 400, replace=False),
-                                     np.argsort(lens)[-24:]]))    # include every dense row
-    check_tol(p.A, p.B, C, rows=rows)
+    check_tol(p.A, p.B, C)
     A, B = synth.dyadic_twin(p.A, 128, 17)
-    C, _ = run_escs(torch_cuda, A, B, **prm)
-    ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B, rows=rows)
-    assert np.array_equal(C[rows].astype(np.float64), ref)
+    C, _ = run_path(torch_cuda, A, B, packed, ufi=info["h"], T=info["T"], cta_warps=info["cta_warps"],
+                    ufk=info["ufk"], colf=info["colf"], tile_order=info["tile_order"])
+    check_exact(A, B, C)
     assert info["n_tiles"] > 0 and info["n_heavy"] > 0
 
 
@@ -225,20 +240,18 @@ def test_rowblock_shards_stitch(torch_cuda):
     check_tol(p.A, p.B, np.concatenate(parts))
 
 
-def test_c5_full_size_sampled(torch_cuda):
-    """C5 (131072^2 at 99.5%, bCols 128) in the bench's launch configuration:
-    sampled rows against the oracle (G2) and the dyadic twin exactly."""
+@pytest.mark.parametrize("packed", [1, 0])
+def test_c5_full_size(torch_cuda, packed):
+    """C5 (131072^2 at 99.5%, bCols 128) in the bench's launch configuration
+    (parameter-table plan: above the tuner's 8M-nonzero cap), every row:
+    G2 on the real values and exact on the dyadic twin."""
     p = synth.config("c5")
-    C, pl = run_escs(torch_cuda, p.A, p.B)
-    rng = np.random.default_rng(1)
-    rows = np.unique(np.concatenate([rng.choice(p.A.m, 512, replace=False),
-                                     [0, p.A.m - 1]]))
-    check_tol(p.A, p.B, C, rows=rows)
-    assert np.all(np.isfinite(C))
+    C, pl = run_path(torch_cuda, p.A, p.B, packed)
+    check_tol(p.A, p.B, C)
+    del C
     A, B = synth.dyadic_twin(p.A, 128, 5)
-    C, _ = run_escs(torch_cuda, A, B)
-    ref = oracle.spmm(A.m, A.k, A.rowptr, A.colidx, A.vals, B, rows=rows)
-    assert np.array_equal(C[rows].astype(np.float64), ref)
+    C, _ = run_path(torch_cuda, A, B, packed)
+    check_exact(A, B, C)
 
 
 def test_pdl_stream_order_with_neighbours(torch_cuda):
@@ -529,19 +542,21 @@ def test_group_graph_capture(torch_cuda):
 
 def test_suite_bench_launch_configuration(torch_cuda):
     """The whole default bench step as bench.py times it: configs[1]+[2]
-    (90 layers), throughput-autotuned plans (autotune = 2, what the
-    multi-stream step runs), layers LPT-partitioned over 16 streams forked
-    from / joined into one stream, PDL chains on each, repeated; every C is
-    bitwise equal to a one-stream run of the same plans and within the G2
-    gate of the oracle."""
+    (90 layers), packed-objective autotuned plans (UFi searched), escs_pack
+    once, escs_spmm_packed per layer on one stream, and the same plans with
+    the layers LPT-partitioned over 16 streams (the multi-stream figure),
+    repeated.  Every one of the 90 C's: bitwise equal between the two
+    launch configurations, within G2 of the oracle, and bit-exact on the
+    dyadic twin packed with the same plan (plans depend only on the pattern)."""
     torch = torch_cuda
     from paper_2506_15174_b200 import escs, shard
     probs = synth.suite()
     dev = []
     for p in probs:
         A = p.A
-        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=2)
-        dev.append((pl, torch.from_numpy(A.vals).cuda(), torch.from_numpy(p.B).cuda(),
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, p.bcols, autotune=1, packed=1)
+        pk = escs.escs_pack(pl, torch.from_numpy(A.vals).cuda())
+        dev.append((pl, pk, torch.from_numpy(p.B).cuda(),
                     torch.full((A.m, p.bcols), float("nan"), device="cuda"),
                     torch.full((A.m, p.bcols), float("nan"), device="cuda")))
     main = torch.cuda.Stream()
@@ -554,16 +569,25 @@ def test_suite_bench_launch_configuration(torch_cuda):
             s.wait_event(fork)
         for g, s in zip(groups, lanes):
             for i in g:
-                pl, v, b, c, _ = dev[i]
-                escs.escs_spmm(pl, v, b, c, stream=s)
+                pl, pk, b, c, _ = dev[i]
+                escs.escs_spmm_packed(pl, pk, b, c, stream=s)
         for s in lanes[1:]:
             j = torch.cuda.Event()
             j.record(s)
             main.wait_event(j)
-    for pl, v, b, _, c1 in dev:
-        escs.escs_spmm(pl, v, b, c1, stream=main)
+    for _ in range(2):
+        for pl, pk, b, _, c1 in dev:
+            escs.escs_spmm_packed(pl, pk, b, c1, stream=main)
     torch.cuda.synchronize()
-    for p, (_, _, _, c4, c1) in zip(probs, dev):
-        assert torch.equal(c4, c1), p.name
-    for p, (_, _, _, c4, _) in list(zip(probs, dev))[::9]:
-        check_tol(p.A, p.B, c4.cpu().numpy())
+    hs = {}
+    for p, (pl, pk, b, c16, c1) in zip(probs, dev):
+        assert torch.equal(c16, c1), p.name
+        check_tol(p.A, p.B, c1.cpu().numpy())
+        hs[pl.info["h"]] = hs.get(pl.info["h"], 0) + 1
+        Ad, Bd = synth.dyadic_twin(p.A, p.bcols, 91)
+        pkd = escs.escs_pack(pl, torch.from_numpy(Ad.vals).cuda())
+        Cd = torch.empty(p.A.m, p.bcols, device="cuda")
+        escs.escs_spmm_packed(pl, pkd, torch.from_numpy(Bd).cuda(), Cd)
+        torch.cuda.synchronize()
+        check_exact(Ad, Bd, Cd.cpu().numpy())
+    print("UFi mix of the bench plans:", hs)
