@@ -46,7 +46,9 @@ enum {
 
 #define ESCS_PLAN_VERSION 1
 #define ESCS_MAX_BCOLS 256     /* largest supported N (bCols)                    */
-#define ESCS_MAX_UFI 4         /* largest UFi the device kernels are built for   */
+#define ESCS_MAX_UFI 8         /* largest UFi of the device kernels: 4 for the CSR-value
+                                  walk (escs_spmm), 8 for the packed record walk
+                                  (escs_spmm_packed; UFi 1-4, 6 and 8 are built)    */
 
 typedef struct escs_plan_impl *escs_plan_t;   /* opaque, library-owned */
 
@@ -205,7 +207,8 @@ int escs_last_error(const char **msg);
 
 typedef struct {
     int32_t ufi;          /* panel height h = UFi, 0 = auto; 1..16 for
-                             host-only plans, 1..ESCS_MAX_UFI for device plans   */
+                             host-only plans; device plans: 1..4 (escs_spmm),
+                             1..4, 6, 8 with packed = 1 (escs_spmm_packed)     */
     int32_t T;            /* max gcols per item (balanced tiles), 0 = auto      */
     int32_t host_only;    /* 1: build host arrays only (no CUDA), for parity     */
     int32_t cta_warps;    /* warps per CTA tile, 0 = auto, else 1..16            */

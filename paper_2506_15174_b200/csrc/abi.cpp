@@ -139,10 +139,12 @@ bool upload(escs_plan_impl* P) {
     // packed gcols (column | pattern << 27) and items {panel, gcol_begin,
     // gcol_end, slot_begin}: the kernel needs no group records (Reading R1:
     // a panel's value slots are contiguous in stream order).
+    // (UFi 5..8, record walk only: col | mask << 24, k < 2^24)
+    const int shift = h <= 4 ? 27 : 24;
     std::vector<int32_t> gpk(G);
     for (int64_t g = 0; g < NG; g++)
         for (int32_t c = ph.grp_col_ptr[g]; c < ph.grp_col_ptr[g + 1]; c++)
-            gpk[c] = ph.gcol[c] | (ph.grp_mask[g] << 27);
+            gpk[c] = (int32_t)((uint32_t)ph.gcol[c] | ((uint32_t)ph.grp_mask[g] << shift));
     const int64_t NS = ph.slot_item.size();
     std::vector<int32_t> items(4 * NS, 0);
     for (int64_t k = 0; k < NS; k++) {
@@ -285,6 +287,10 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         p.variant = 2;
     if (!host_only && k >= (1 << 27)) {
         fail(ESCS_ERR_UNSUPPORTED, "device plans need k < 2^27 (packed column words)");
+        return nullptr;
+    }
+    if (!host_only && p.h > 4 && k >= (1 << 24)) {
+        fail(ESCS_ERR_UNSUPPORTED, "device plans with UFi > 4 need k < 2^24 (packed column words)");
         return nullptr;
     }
     if (p.variant != 1) {
@@ -618,11 +624,13 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     // before W never reaches (profiles/r2_notes.md).  Items per panel
     // {1, 3, 8, 24} x tile width {auto, 4, 16}, from the expected panel stream
     // k(1 - s^h) of a uniformly pruned matrix.
-    if (packed && !(ep && ep->ufi)) {
+    if (packed) {
         const double dens = (double)nnz / ((double)m * (double)k);
         float best_h1 = best->params.h == 1 ? tb : kFailed;
-        for (int h : {1, 2, 3, 4}) {
-            if (h == 2) {
+        const bool fixed_h = ep && ep->ufi;   // an explicit UFi: the joint (T, W) grid at that UFi
+        for (int h : {1, 2, 3, 4, 6, 8}) {
+            if (fixed_h ? h != ep->ufi : (h > 4 && dens < 0.15)) continue;   // UFi 6/8 where p is large
+            if (h == 2 && !fixed_h) {
                 // UFi > 1 must beat the best UFi = 1 plan by a margin: its
                 // split panels combine through the workspace, which the hot
                 // timing undercounts on a cold L2 (bench steps flush it)
@@ -772,6 +780,9 @@ static int spmm_common(escs_plan_t plan, const float* vals, const float* B, floa
                                       " differs from the plan's device " +
                                       std::to_string(plan->device));
     const bool vec_ok = aligned16(B) && aligned16(C);
+    if (!packed && plan->dev.h > 4)
+        return fail(ESCS_ERR_UNSUPPORTED, "the CSR-value walk (escs_spmm) is built for UFi <= 4; "
+                                          "run this plan through escs_pack + escs_spmm_packed");
     if (packed && !(vec_ok && plan->dev.variant == 1))
         return fail(ESCS_ERR_UNSUPPORTED, "escs_spmm_packed needs 16-byte aligned B and C and a "
                                           "vector-kernel plan (bCols in {4,8,16,32,64,128,256})");

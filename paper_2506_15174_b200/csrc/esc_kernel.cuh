@@ -464,6 +464,8 @@ enum Mode { kCsr = 0, kProbe = 1, kRec = 2, kRecProbe = 3 };
 //   UFi = 1      int2 {col, value}                              ( 8 bytes)
 //   UFi = 2, 3   int4 {col | mask << 27, w_0, .., w_{h-1}, 0..}  (16 bytes)
 //   UFi = 4      2 x int4 {col | mask << 27, w_0, w_1, w_2}, {w_3, 0, 0, 0}
+//   UFi = 6      2 x int4 {col | mask << 24, w_0 .. w_5, 0}      (32 bytes)
+//   UFi = 8      3 x int4 {col | mask << 24, w_0 .. w_7, 0, 0, 0} (48 bytes)
 // A (sub-)warp reads its column's record with ONE broadcast load (all lanes
 // of the sub-warp the same address: one L1 wavefront), so the column index,
 // the pattern and every value arrive together: no shuffles, no slot map, no
@@ -471,17 +473,30 @@ enum Mode { kCsr = 0, kProbe = 1, kRec = 2, kRecProbe = 3 };
 // reused in registers for every row of the pattern (§3.3.2).
 template <int H>
 struct RecFmt {
-    static constexpr int W = H == 1 ? 2 : (H <= 3 ? 4 : 8);   // int words per record
+    // int words per record: {word0, w_0 .. w_{h-1}} padded to 2, 4, 8 or 12
+    static constexpr int W = H == 1 ? 2 : (H <= 3 ? 4 : (H <= 7 ? 8 : 12));
+    // word0 = col | mask << Shift: 27 for UFi <= 4 (the plan's packed gcol
+    // word, k < 2^27), 24 for UFi 5..8 (k < 2^24)
+    static constexpr int Shift = H <= 4 ? kColBits : 24;
+    static constexpr int ColMask = (1 << Shift) - 1;
+    static constexpr int Words = H == 1 ? 2 : 1 + H;   // words the walk reads
 };
 
-template <int RW>
+template <int RW, int NW>
 __device__ __forceinline__ void ld_rec(int (&r)[RW], const int* q) {
     if constexpr (RW == 2) {
         asm volatile("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "l"(q));
     } else {
-        asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(q));
-        if constexpr (RW == 8) asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(r[4]) : "l"(q + 4));
+#pragma unroll
+        for (int v = 0; v < NW / 4; v++)
+            asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(r[4 * v]), "=r"(r[4 * v + 1]), "=r"(r[4 * v + 2]), "=r"(r[4 * v + 3])
+                         : "l"(q + 4 * v));
+        constexpr int R = NW % 4, B0 = NW - R;
+        if constexpr (R >= 2)
+            asm volatile("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(r[B0]), "=r"(r[B0 + 1]) : "l"(q + B0));
+        if constexpr (R == 1 || R == 3)
+            asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(r[NW - 1]) : "l"(q + NW - 1));
     }
 }
 
@@ -501,8 +516,8 @@ __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, in
 #pragma unroll
     for (int u = 0; u < U; u++) {
         const int idx = i + u * S + sub;
-        ld_rec<RW>(r[u], rec + (size_t)(TAIL ? min(idx, end - 1) : idx) * RW);
-        if (TAIL && H > 1 && idx >= end) r[u][0] &= kColMask;   // no pattern rows
+        ld_rec<RW, RecFmt<H>::Words>(r[u], rec + (size_t)(TAIL ? min(idx, end - 1) : idx) * RW);
+        if (TAIL && H > 1 && idx >= end) r[u][0] &= RecFmt<H>::ColMask;   // no pattern rows
     }
     if constexpr (!TAIL) {
         // the record lines two batches ahead into L1: with a cold L2 (the
@@ -515,7 +530,7 @@ __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, in
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        const int col = H == 1 ? r[u][0] : (r[u][0] & kColMask);
+        const int col = H == 1 ? r[u][0] : (r[u][0] & RecFmt<H>::ColMask);
         Map::load_pol(b[u], p.B + (size_t)col * N, lj, pol_b);
     }
 #pragma unroll
@@ -526,7 +541,7 @@ __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, in
         } else if constexpr (H == 1) {
             if (!TAIL || i + u * S + sub < end) fma_row<F>(acc[0], __int_as_float(r[u][1]), b[u]);
         } else {
-            const unsigned mk = (unsigned)r[u][0] >> kColBits;
+            const unsigned mk = (unsigned)r[u][0] >> RecFmt<H>::Shift;
 #pragma unroll
             for (int row = 0; row < H; row++)
                 if ((mk >> row) & 1u) fma_row<F>(acc[row], __int_as_float(r[u][1 + row]), b[u]);
@@ -845,11 +860,19 @@ __global__ void ESC_CSR_BOUNDS esc_spmm_kernel(KParams p) {
 // flight); a register target of 72 keeps 8 loads in flight at 7 CTAs of 4
 // warps per SM: 512x4608@70% bCols 128, UFi 3: 24.6 us -> 19.1 us
 // (profiles/r2_notes.md, "record walk register target").
+// Wider register tiles (H x F accumulators beyond 32) get the target raised
+// with them (UFi 6/8, 16 columns per lane), up to 128.
 #ifndef ESC_REC_MAXREG
 #define ESC_REC_MAXREG 72
 #endif
+template <int H, class Map>
+struct RecRegs {
+    static constexpr int acc = H * Map::F;
+    static constexpr int value = acc <= 32 ? ESC_REC_MAXREG
+                                           : ((acc + 48 + 7) / 8 * 8 > 128 ? 128 : (acc + 48 + 7) / 8 * 8);
+};
 #if ESC_REC_MAXREG > 0
-#define ESC_REC_BOUNDS __maxnreg__(ESC_REC_MAXREG)
+#define ESC_REC_BOUNDS __maxnreg__((RecRegs<H, Map>::value))
 #else
 #define ESC_REC_BOUNDS __launch_bounds__(512)
 #endif

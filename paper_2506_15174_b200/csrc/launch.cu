@@ -29,23 +29,23 @@ __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict
     constexpr int RW = RecFmt<H>::W;
     grid_dep_wait();
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < G; j += gridDim.x * blockDim.x) {
-        const int pk = gpk[j];
+        const int pk = gpk[j];   // the plan's word: col | mask << RecFmt<H>::Shift
         if constexpr (H == 1) {
             *reinterpret_cast<int2*>(out + (size_t)j * 2) =
-                make_int2(pk & kColMask, __float_as_int(vals[j]));
+                make_int2(pk & RecFmt<1>::ColMask, __float_as_int(vals[j]));
         } else {
             int w[RW];
 #pragma unroll
             for (int q = 0; q < RW; q++) w[q] = 0;
             w[0] = pk;
-            const unsigned mk = (unsigned)pk >> kColBits;
+            const unsigned mk = (unsigned)pk >> RecFmt<H>::Shift;
             int s = vbase[j];
 #pragma unroll
             for (int r = 0; r < H; r++)
                 if ((mk >> r) & 1u) w[1 + r] = __float_as_int(vals[slot[s++]]);
             int4* o = reinterpret_cast<int4*>(out + (size_t)j * RW);
-            o[0] = make_int4(w[0], w[1], w[2], w[3]);
-            if constexpr (RW == 8) o[1] = make_int4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+            for (int v = 0; v < RW / 4; v++) o[v] = make_int4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
         }
     }
 }
@@ -131,9 +131,10 @@ int launch_spin(void* stream, long long cycles) {
 }
 
 bool kernel_supported(int h, int bcols, int variant, int ufk, int colf, bool packed) {
-    if (h < 1 || h > 4 || bcols < 1 || bcols > 256) return false;
-    if (packed)   // the record walk: vector lane map only
+    if (h < 1 || h > 8 || bcols < 1 || bcols > 256) return false;
+    if (packed)   // the record walk: vector lane map only; UFi 1-4, 6, 8
         return variant == 1 && select_kernel(h, bcols, true, ufk, kern::kRec, colf) != nullptr;
+    if (h > 4) return false;   // the CSR-value walk: UFi 1-4
     return select_kernel(h, bcols, variant == 1, ufk, kern::kCsr, colf) != nullptr &&
            select_kernel(h, bcols, false, ufk, kern::kCsr, 0) != nullptr;
 }
@@ -203,7 +204,7 @@ int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed) {
 }
 
 int64_t packed_words(const DevPlan& dp) {
-    const int rw = dp.h == 1 ? 2 : (dp.h <= 3 ? 4 : 8);
+    const int rw = dp.h == 1 ? 2 : (dp.h <= 3 ? 4 : (dp.h <= 7 ? 8 : 12));   // kern::RecFmt<h>::W
     return (int64_t)dp.G * rw;
 }
 
@@ -218,6 +219,8 @@ int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* strea
         case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
         case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
         case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 6: kern::esc_pack_rec_kernel<6><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 8: kern::esc_pack_rec_kernel<8><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
         default: return (int)cudaErrorInvalidConfiguration;
     }
     return (int)cudaGetLastError();

@@ -16,7 +16,7 @@ def main():
     flt = sys.argv[1] if len(sys.argv) > 1 else ""
     for log in sorted(glob.glob(os.path.join(BUILD, "k_*.cu.o.log"))):
         txt = open(log).read()
-        for m in re.finditer(r"Compiling entry function '(\w+)'.*?\n(.*?)\n.*?Used (\d+) registers", txt, re.S):
+        for m in re.finditer(r"Compiling entry function '(\w+)'(.*?)Used (\d+) registers", txt, re.S):
             name, spill, regs = m.group(1), m.group(2), m.group(3)
             k = re.search(r"esc_(?:spmm|rec)_kernelILi(\d)ENS0_(\d+)(VecMap|ScalarMap)ILi(\d+)E(?:Li(\d+)E)?EELi(\d)ELi(\d)E", name)
             if not k:
@@ -25,7 +25,10 @@ def main():
             sp = re.search(r"(\d+) bytes spill stores", spill)
             line = f"h={h} {mp} L={L} F={F} U={U} {MODES[md]:8s} regs={regs} spill={sp.group(1) if sp else '?'}"
             if flt in line:
-                print(line)
+                try:
+                    print(line)
+                except BrokenPipeError:
+                    return
 
 
 if __name__ == "__main__":
