@@ -881,6 +881,11 @@ def run_escs(args):
                     "frac": float(probe_ms.sum() / kern_ms.sum()),
                     "what": "t_probe / t_kernel summed over the step's launches (escs_gather_probe[_packed]: same walk and "
                             "B-row gathers, no FMAs)"}},
+            "cold_us_per_launch": {"what": "mean per-launch duration in the timed one-stream steps (L2 flushed "
+                                           "before each step), in problem order",
+                                   "names": [p.name for p, _ in shard_problems],
+                                   "us": [round(1e3 * float(x), 3) for x in per_prob],
+                                   "ufi": [inf["h"] for inf in infos]},
             "gpu_launches": nprob * K,
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,

@@ -587,56 +587,146 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     const bool concurrent = q.autotune == 2;
     const bool packed = q.packed != 0;
     q.autotune = 0;
-    escs_plan_t best = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+    escs_plan_t first = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
     // Throughput plans launch without programmatic dependent launch: with
     // many streams sharing the SMs, CTAs that start early and wait on the
     // previous grid hold SM slots the other streams' layers could use (suite
     // on 16 streams +2%; profiles/r1_notes.md)
-    if (best && concurrent) best->dev.pdl = false;
-    if (!best || nnz > 8000000) return best;   // large problems: many waves, heuristic holds
-    if (packed && best->dev.variant != 1) return best;   // the record walk needs the vector map
+    if (first && concurrent) first->dev.pdl = false;
+    if (!first || nnz > 8000000) return first;   // large problems: many waves, heuristic holds
+    if (packed && first->dev.variant != 1) return first;   // the record walk needs the vector map
     TuneBufs bufs(m, k, nnz, bCols, concurrent);
-    if (!bufs.ok) return best;
+    if (!bufs.ok) return first;
+    struct Cand {
+        escs_plan_t P = nullptr;
+        float t = kFailed;
+    };
     auto timed = [&](escs_plan_t P) -> float {
         return concurrent ? time_plans_concurrent(P, bufs, packed) : time_plan(P, bufs, packed);
     };
-    float tb = timed(best);
-    auto consider = [&](escs_params c) {
+    auto build = [&](escs_params c) -> Cand {
         escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
         if (!P) {
             clear_error();
-            return;
+            return {};
         }
         if (concurrent) P->dev.pdl = false;
-        const float t = timed(P);
-        if (t < tb) {
-            escs_free(best);
-            best = P;
-            tb = t;
+        return {P, timed(P)};
+    };
+    auto keep = [](Cand& cur, Cand x) {   // cur = the faster of cur and x (the other is freed)
+        if (!x.P) return;
+        if (x.t < cur.t) {
+            if (cur.P) escs_free(cur.P);
+            cur = x;
         } else {
-            escs_free(P);
+            escs_free(x.P);
         }
     };
-    // stage 0 (record walk): UFi jointly with the item size and the tile
-    // width -- the paper's tuner searches UFi first; on B200 the
-    // best UFi > 1 plans need short items in narrow tiles (many warps per
-    // panel, combined through the workspace), which a descent that fixes T
-    // before W never reaches (profiles/r2_notes.md).  Items per panel
-    // {1, 3, 8, 24} x tile width {auto, 4, 16}, from the expected panel stream
-    // k(1 - s^h) of a uniformly pruned matrix.
-    if (packed) {
+    // the parameters of a plan as an escs_params candidate base
+    auto params_of = [&](escs_plan_t P) {
+        escs_params c = q;
+        c.ufi = P->params.h;
+        c.T = P->params.T;
+        c.cta_warps = P->params.cta_warps;
+        c.ufk = P->params.ufk;
+        c.colf = P->dev.variant == 1 ? P->params.colf : 0;
+        return c;
+    };
+    // Coordinate descent from a start plan at a fixed UFi: the item size T
+    // (tile width then follows automatically), the tile width W, UFk, the bCols
+    // coarsening factor, the tile order.
+    auto refine = [&](Cand cur) -> Cand {
+        if (!(ep && ep->T)) {   // stage 1: item size
+            const double nP = (double)cur.P->host.header[7];
+            const double sp = nP > 0 ? (double)cur.P->host.header[9] / nP : 0.0;
+            std::vector<int> cand;
+            const int T0 = cur.P->params.T;
+            const std::vector<double> fs = packed ? std::vector<double>{0.5, 0.7, 1.4, 2.0}
+                                                  : std::vector<double>{0.25, 0.35, 0.5, 0.7, 1.4, 2.0, 3.0, 5.0};
+            const std::vector<int> pers = packed ? std::vector<int>{1, 2, 4} : std::vector<int>{1, 2, 3, 4, 6, 8};
+            for (double f : fs) cand.push_back(std::max(8, (int)(T0 * f)));
+            for (int per : pers)
+                if (sp >= 1.0) cand.push_back(std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / per)));
+            std::sort(cand.begin(), cand.end());
+            cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+            const escs_params base = params_of(cur.P);
+            for (int T : cand) {
+                if (T == T0) continue;
+                escs_params c = base;
+                c.T = T;
+                c.cta_warps = (ep && ep->cta_warps) ? ep->cta_warps : 0;   // auto width for the new T
+                keep(cur, build(c));
+            }
+        }
+        // stage 2: tile width.  Whole panels are packed per tile, so W sets
+        // both the warps per CTA and the tile count; the intermediate widths
+        // let a layer land on one full wave of the 148 SMs (2048x512@70% b128:
+        // 14 warps -> 147 tiles, 9.4 us vs 10.2 us at 16 warps -> 128 tiles;
+        // profiles/r1_notes.md)
+        if (!(ep && ep->cta_warps)) {
+            const escs_params base = params_of(cur.P);
+            for (int W : {4, 6, 8, 10, 12, 14, 16}) {
+                if (W == base.cta_warps) continue;
+                escs_params c = base;
+                c.cta_warps = W;
+                keep(cur, build(c));
+            }
+        }
+        if (!(ep && ep->ufk)) {   // stage 3: rows in flight
+            const escs_params base = params_of(cur.P);
+            for (int U : {2, 4, 8}) {
+                if (U == base.ufk || bCols < 32 || (U == 2 && !packed)) continue;
+                escs_params c = base;
+                c.ufk = U;
+                keep(cur, build(c));
+            }
+        }
+        // stage 4: B columns per lane (bCols coarsening of the vector lane map;
+        // wider per-lane tiles trade shuffles or broadcasts per gathered row
+        // for fewer lanes); the CSR walk has the alternatives at UFi = 1 only
+        if (!(ep && ep->colf) && (cur.P->params.h == 1 || packed) && cur.P->dev.variant == 1) {
+            const escs_params base = params_of(cur.P);
+            for (int F : {4, 8, 16}) {
+                if (F == base.colf) continue;
+                for (int U : {base.ufk, 4, 2}) {
+                    escs_params c = base;
+                    c.ufk = U;
+                    c.colf = F;
+                    if (!escs::kernel_supported(c.ufi, bCols, 1, U, F, packed)) continue;
+                    keep(cur, build(c));
+                    break;
+                }
+            }
+        }
+        if (!(ep && ep->tile_order)) {   // stage 5: tile order
+            escs_params c = params_of(cur.P);
+            c.tile_order = cur.P->params.tile_order == 2 ? 1 : 2;
+            keep(cur, build(c));
+        }
+        return cur;
+    };
+
+    Cand best;
+    if (!packed) {
+        best = refine({first, timed(first)});
+    } else {
+        // Stage 0 (record walk): UFi jointly with the item size and the tile
+        // width -- the paper's tuner searches UFi first; on B200
+        // the best UFi > 1 plans need short items in narrow tiles (many warps
+        // per panel, combined through the workspace), which a descent that
+        // fixes T before W never reaches (profiles/r2_notes.md).  Items per
+        // panel {1, 3, 8, 24} x tile width {auto, 4, 16}, from the expected
+        // panel stream k(1 - s^h) of a uniformly pruned matrix.  Then the
+        // best UFi and UFi = 1 are each refined; a UFi > 1 plan is kept only
+        // if it beats the refined UFi = 1 plan by 3% (its split panels combine
+        // through the workspace, which the hot timing undercounts on a cold
+        // L2: bench steps flush it).
+        Cand per_h[9];
+        per_h[first->params.h] = {first, timed(first)};
         const double dens = (double)nnz / ((double)m * (double)k);
-        float best_h1 = best->params.h == 1 ? tb : kFailed;
-        const bool fixed_h = ep && ep->ufi;   // an explicit UFi: the joint (T, W) grid at that UFi
+        const bool fixed_h = ep && ep->ufi;
         for (int h : {1, 2, 3, 4, 6, 8}) {
             if (fixed_h ? h != ep->ufi : (h > 4 && dens < 0.15)) continue;   // UFi 6/8 where p is large
-            if (h == 2 && !fixed_h) {
-                // UFi > 1 must beat the best UFi = 1 plan by a margin: its
-                // split panels combine through the workspace, which the hot
-                // timing undercounts on a cold L2 (bench steps flush it)
-                best_h1 = std::min(best_h1, best->params.h == 1 ? tb : kFailed);
-                if (best->params.h == 1) tb *= 0.97f;
-            }
             const double sp = (double)k * (1.0 - std::pow(1.0 - dens, h));
             const int pw[6][2] = {{1, 0}, {3, 0}, {8, 4}, {8, 16}, {24, 4}, {24, 16}};
             for (const auto& x : pw) {
@@ -645,100 +735,30 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
                 c.ufi = h;
                 if (!(ep && ep->T)) c.T = std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / x[0]));
                 if (!(ep && ep->cta_warps)) c.cta_warps = x[1];
-                consider(c);
+                keep(per_h[h], build(c));
             }
         }
-        if (best->params.h == 1 && best_h1 < kFailed) tb = best_h1;   // undo the margin
-    }
-    const int h = best->params.h;
-    const int F_best = best->dev.variant == 1 ? best->params.colf : 0;
-    // stage 1: item size T (tile width follows automatically)
-    if (!(ep && ep->T)) {
-        const double nP = (double)best->host.header[7];
-        const double sp = nP > 0 ? (double)best->host.header[9] / nP : 0.0;
-        std::vector<int> cand;
-        const int T0 = best->params.T;
-        for (double f : {0.25, 0.35, 0.5, 0.7, 1.4, 2.0, 3.0, 5.0}) cand.push_back(std::max(8, (int)(T0 * f)));
-        for (int per : {1, 2, 3, 4, 6, 8})
-            if (sp >= 1.0) cand.push_back(std::max(8, (int)std::ceil((sp + 3 * std::sqrt(sp)) / per)));
-        std::sort(cand.begin(), cand.end());
-        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-        for (int T : cand) {
-            if (T == T0) continue;
-            escs_params c = q;
-            c.ufi = h;
-            c.T = T;
-            c.colf = F_best;
-            c.ufk = best->params.ufk;
-            consider(c);
-        }
-    }
-    // stage 2: tile width.  Whole panels are packed per tile, so W sets both
-    // the warps per CTA and the tile count; the intermediate widths let a
-    // layer land on one full wave of the 148 SMs (2048x512@70% b128: 14 warps
-    // -> 147 tiles, 9.4 us vs 10.2 us at 16 warps -> 128 tiles; gpurun
-    // wave_sweep, profiles/r1_notes.md)
-    if (!(ep && ep->cta_warps)) {
-        const int W0 = best->params.cta_warps, T = best->params.T;
-        for (int W : {4, 6, 8, 10, 12, 14, 16}) {
-            if (W == W0) continue;
-            escs_params c = q;
-            c.ufi = h;
-            c.T = T;
-            c.cta_warps = W;
-            c.colf = F_best;
-            c.ufk = best->params.ufk;
-            consider(c);
-        }
-    }
-    // stage 3: rows in flight
-    if (!(ep && ep->ufk)) {
-        const int U0 = best->params.ufk;
-        for (int U : {2, 4, 8}) {
-            if (U == U0 || bCols < 32 || (U == 2 && !packed)) continue;
-            escs_params c = q;
-            c.ufi = h;
-            c.T = best->params.T;
-            c.cta_warps = best->params.cta_warps;
-            c.colf = F_best;
-            c.ufk = U;
-            consider(c);
-        }
-    }
-    // stage 4: B columns per lane (bCols coarsening of the vector lane map;
-    // wider per-lane tiles trade shuffles per gathered row for fewer lanes);
-    // the CSR walk has the alternative factors at UFi = 1 only
-    if (!(ep && ep->colf) && (best->params.h == 1 || packed) && best->dev.variant == 1) {
-        const int F0 = best->params.colf;
-        for (int F : {4, 8, 16}) {
-            if (F == F0) continue;
-            for (int U : {best->params.ufk, 4, 2}) {
-                escs_params c = q;
-                c.ufi = best->params.h;
-                c.T = best->params.T;
-                c.cta_warps = best->params.cta_warps;
-                c.ufk = U;
-                c.colf = F;
-                if (!escs::kernel_supported(c.ufi, bCols, 1, U, F, packed)) continue;
-                consider(c);
-                break;
+        int hb = 0;
+        for (int h = 1; h <= 8; h++)
+            if (per_h[h].P && (!hb || per_h[h].t < per_h[hb].t)) hb = h;
+        for (int h = 1; h <= 8; h++)   // keep only the best UFi and UFi = 1
+            if (per_h[h].P && h != hb && h != 1) {
+                escs_free(per_h[h].P);
+                per_h[h] = {};
             }
+        Cand r1 = per_h[1].P ? refine(per_h[1]) : Cand{};
+        Cand rb = (hb != 1 && per_h[hb].P) ? refine(per_h[hb]) : Cand{};
+        if (rb.P && (!r1.P || rb.t < 0.97f * r1.t)) {
+            if (r1.P) escs_free(r1.P);
+            best = rb;
+        } else {
+            if (rb.P) escs_free(rb.P);
+            best = r1;
         }
     }
-    // stage 5: tile order (panel order vs panels by longest item)
-    if (!(ep && ep->tile_order)) {
-        escs_params c = q;
-        c.ufi = best->params.h;
-        c.T = best->params.T;
-        c.cta_warps = best->params.cta_warps;
-        c.ufk = best->params.ufk;
-        c.colf = best->dev.variant == 1 ? best->params.colf : 0;
-        c.tile_order = best->params.tile_order == 2 ? 1 : 2;
-        consider(c);
-    }
-    best->autotuned = true;
+    best.P->autotuned = true;
     clear_error();
-    return best;
+    return best.P;
 }
 
 escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
