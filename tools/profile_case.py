@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--case", default=None, help="a problem name from bench.py's workloads")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="plan with the parameter table (default: autotuned, as bench.py)")
+    ap.add_argument("--csr", action="store_true",
+                    help="the CSR-value walk (escs_spmm) instead of the packed record walk bench.py times")
+    ap.add_argument("--ufi", type=int, default=0, help="force UFi (0: tuned)")
     ap.add_argument("--objective", type=int, default=1,
                     help="autotune objective: 1 latency (serial/per-case plans), 2 concurrent "
                          "throughput (the plans bench.py's multi-stream step runs)")
@@ -48,9 +51,11 @@ def main():
         r0, r1 = synth.shard_bounds(A.m, world, rank)
         A = synth.row_block(A, r0, r1)
     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
-                           autotune=a.objective if a.autotune else 0)
+                           autotune=(a.objective if a.autotune and A.nnz <= 8_000_000 else 0),
+                           packed=0 if a.csr else 1, ufi=a.ufi)
     print(pl.info, flush=True)
     dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
+    pk = None if a.csr else escs.escs_pack(pl, dv)
     dC = torch.empty(A.m, B.shape[1], device="cuda")
     sink = torch.empty(pl.info["n_tiles"] * 32 * pl.info["cta_warps"], device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -59,9 +64,14 @@ def main():
         torch.cuda._sleep(2_000_000)   # host runs ahead: events bracket the kernel only
         s.record()
         if a.probe:
-            escs.escs_gather_probe(pl, dB, sink)
-        else:
+            if pk is None:
+                escs.escs_gather_probe(pl, dB, sink)
+            else:
+                escs.escs_gather_probe_packed(pl, pk, dB, sink)
+        elif pk is None:
             escs.escs_spmm(pl, dv, dB, dC)
+        else:
+            escs.escs_spmm_packed(pl, pk, dB, dC)
         e.record()
         torch.cuda.synchronize()
         print(f"rep {i}: {s.elapsed_time(e) * 1e3:.1f} us", flush=True)

@@ -6,7 +6,7 @@ import json
 import sys
 
 
-def main(src, dst, workload="transformer"):
+def main(src, dst, workload="suite", case=None):
     rows = list(csv.reader(open(src)))
     hdr, data = None, []
     for r in rows:
@@ -17,14 +17,25 @@ def main(src, dst, workload="transformer"):
             data.append(dict(zip(hdr, r)))
     per = {}
     for d in data:
-        if "esc_spmm_kernel" not in d["Kernel Name"]:
+        if "esc_spmm_kernel" not in d["Kernel Name"] and "esc_rec_kernel" not in d["Kernel Name"]:
             continue
         per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     launches = len(per)
-    tot = sum(v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in per.values())
+    dram = [v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)
+            for _, v in sorted(per.items(), key=lambda kv: int(kv[0]))]
     out = {"workload": workload, "launches": launches,
-           "dram_bytes_per_launch": tot / max(launches, 1),
+           "step_mean_dram_bytes_per_launch": sum(dram) / max(launches, 1),
            "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one bench step ({src})"}
+    if case is not None:
+        # the dominant layer's launch: its index in the workload's problem order
+        import os
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        names = [p.name for p in bench.workload(workload)[0]]
+        idx = names.index(case)
+        out.update(case=case, launch_index=idx, dram_bytes_per_launch=dram[idx])
+    else:
+        out["dram_bytes_per_launch"] = out["step_mean_dram_bytes_per_launch"]
     json.dump(out, open(dst, "w"), indent=1)
     print(out)
 
