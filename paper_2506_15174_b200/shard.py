@@ -59,7 +59,10 @@ def all_gather_rows(C_local, m: int, world: int, group=None):
     buf = torch.zeros((rows_max, n), dtype=C_local.dtype, device=C_local.device)
     buf[:C_local.shape[0]] = C_local
     out = torch.empty((world * rows_max, n), dtype=C_local.dtype, device=C_local.device)
-    dist.all_gather_into_tensor(out, buf, group=group)
+    try:
+        dist.all_gather_into_tensor(out, buf, group=group)
+    except (RuntimeError, NotImplementedError):   # backends without the fused form (gloo + CUDA)
+        dist.all_gather(list(out.split(rows_max)), buf, group=group)
     parts = [out[r * rows_max:r * rows_max + (r1 - r0)] for r, (r0, r1) in enumerate(blocks)]
     return torch.cat(parts, 0)
 
