@@ -309,25 +309,62 @@ def graph_time(torch, fn, stream, min_ms=2.0, reps=11, stats=None):
     return statistics.median(ts)
 
 
-def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs):
+def gather_ceiling(torch, dev, stream):
+    """Measured L2 -> SM random-row gather rate (GB/s): bl_gather_peak gathers
+    hashed 512-byte rows of a 64 MiB L2-resident B with no index loads, values
+    or FMAs, best of 6 lane maps / depths at 64 warps per SM (the same
+    ceiling as profiles/r2_l1_gather_microbench.txt's L2 rows)."""
+    import ctypes
+    from paper_2506_15174_b200.build import BENCH_LIB
+    bl = ctypes.CDLL(BENCH_LIB)
+    bl.bl_gather_peak.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_longlong, ctypes.c_void_p, ctypes.c_void_p]
+    k = 131072
+    B = torch.rand(k, 128, device=dev)
+    sink = torch.zeros(256, device=dev)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ctas, rpw = n_sm * 8, 2048
+    rows = ctas * 8 * rpw
+    best = None
+    for v in range(6):
+        for _ in range(2):
+            assert bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream) == 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            bl.bl_gather_peak(B.data_ptr(), k, v, ctas, rpw, sink.data_ptr(), stream.cuda_stream)
+        b.record(stream)
+        b.synchronize()
+        gbs = 3 * rows * 512 / (a.elapsed_time(b) * 1e-3) / 1e9
+        best = gbs if best is None else max(best, gbs)
+    del B
+    return best
+
+
+def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None):
     """SURVEY §8(d) ceilings of one SpMM (microseconds): compulsory HBM bytes,
-    the FP32 FMA pipe, and the L1 data path every gathered B row crosses
-    (4*bCols bytes per gcol at 128 B/clk/SM; profiles/r2_notes.md §1)."""
+    the FP32 FMA pipe, the L1 data path every gathered B row crosses (4*bCols
+    bytes per gcol at 128 B/clk/SM; profiles/r2_notes.md §1), and -- when
+    the rows come from L2, as random gathers without reuse do -- the measured
+    L2 -> SM random-row gather rate."""
     A, n = p.A, p.bcols
     f = f_mhz * 1e6
     bytes_comp = 8 * A.nnz + 4 * (A.m + 1) + 4 * A.k * n + 4 * A.m * n
-    return {"bytes_comp": bytes_comp,
-            "t_hbm_us": bytes_comp / (hbm_gbs * 1e9) * 1e6,
-            "t_fma_us": A.nnz * n / (n_sm * 128 * f) * 1e6,
-            "t_l1_us": 4.0 * n * G / (n_sm * 128 * f) * 1e6}
+    out = {"bytes_comp": bytes_comp,
+           "t_hbm_us": bytes_comp / (hbm_gbs * 1e9) * 1e6,
+           "t_fma_us": A.nnz * n / (n_sm * 128 * f) * 1e6,
+           "t_l1_us": 4.0 * n * G / (n_sm * 128 * f) * 1e6}
+    if l2_gather_gbs:
+        out["t_l2_us"] = 4.0 * n * G / (l2_gather_gbs * 1e9) * 1e6
+    return out
 
 
 CASE_COLUMNS = ("case", "ufi", "t_escs_us", "t_escs_csr_us", "t_cusparse_us", "t_cublas_us",
                 "t_cublas_tf32_us", "gflops", "eff_GBps", "pct_hbm", "t_hbm_us", "t_fma_us",
-                "t_l1_us", "t_probe_us", "probe_frac", "attainable_frac", "binding")
+                "t_l1_us", "t_l2_us", "t_probe_us", "probe_frac", "attainable_frac", "l2_gather_frac", "binding")
 
 
-def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_csr=True):
+def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_csr=True, l2_gbs=None):
     """Per-case hot-L2 table (the paper's warm protocol): the timed
     packed-record escs plan, the CSR-value walk of the same plan (escs_spmm),
     cuSPARSE (best of 4 algorithms), cuBLAS fp32 / TF32 (dense A), the gather
@@ -383,7 +420,7 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
         del Ad
         inf = d["plan"].info
-        rb = roofline_bounds(p, inf["G"], n_sm, f_mhz, hbm_gbs)
+        rb = roofline_bounds(p, inf["G"], n_sm, f_mhz, hbm_gbs, l2_gbs)
         t_us = 1e3 * t_escs
         # the ceilings are lower bounds on the time (HBM bytes, FMA issue, L1
         # data path); the probe (same walk, no FMAs) is reported beside them
@@ -403,6 +440,7 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
                      "t_probe_us": 1e3 * t_probe if t_probe else None,
                      "probe_frac": (1e3 * t_probe / t_us) if t_probe else None,
                      "attainable_frac": bounds[binding] / t_us, "binding": binding,
+                     "t_l2_us": rb.get("t_l2_us"), "l2_gather_frac": (rb["t_l2_us"] / t_us) if "t_l2_us" in rb else None,
                      "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")}})
     bl.bl_cublas_destroy(cub)
     sel = lambda key: [r[key] for r in rows]
@@ -417,6 +455,7 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         "pct_faster_than_cusparse": 100.0 * np.mean([r["t_cusparse_us"] is not None and r["t_escs_us"] < r["t_cusparse_us"] for r in rows]),
         "pct_faster_than_cublas": 100.0 * np.mean([r["t_escs_us"] < r["t_cublas_us"] for r in rows]),
         "median_attainable_frac": float(np.median(sel("attainable_frac"))),
+        "median_l2_gather_frac": (float(np.median(sel("l2_gather_frac"))) if l2_gbs else None),
         "median_pct_hbm": float(np.median(sel("pct_hbm"))),
         "cases": len(rows),
         "paper_context": "A100: 1.84x vs cuBLAS, 2.27x vs cuSPARSE (abstract P:31); Table 1 geomeans 1.47x / 1.74x",
@@ -830,7 +869,11 @@ def run_escs(args):
         per_prob = kern_ms.mean(axis=0)                # ms per launch, L2 flushed per step
         dom = int(np.argmax(per_prob))
         pd, dd = shard_problems[dom]
-        rb = roofline_bounds(pd, dd["G"], n_sm, f_mhz, hbm)
+        try:
+            l2_gbs = gather_ceiling(torch, device, stream)
+        except (OSError, AssertionError):
+            l2_gbs = None
+        rb = roofline_bounds(pd, dd["G"], n_sm, f_mhz, hbm, l2_gbs)
         t_dom_us = 1e3 * float(per_prob[dom])
         dom_gbs = rb["bytes_comp"] / (t_dom_us * 1e-6) / 1e9
         clocks = clk.summary()
@@ -873,6 +916,11 @@ def run_escs(args):
                                       "what": "4*bCols bytes per gcol (plan G) through 128 B/clk/SM at the max SM clock "
                                               "(profiles/r2_notes.md 1): the ceiling that binds, not HBM"},
                 "t_fma_us": rb["t_fma_us"], "t_hbm_us": rb["t_hbm_us"],
+                "l2_gather_ceiling": None if l2_gbs is None else {
+                    "measured_GBps": l2_gbs, "t_l2_us": rb["t_l2_us"], "frac": rb["t_l2_us"] / t_dom_us,
+                    "what": "4*bCols bytes per gcol at the measured L2->SM random 512-byte-row gather rate "
+                            "(bl_gather_peak in libescs_bench.so, measured in this run): the ceiling of a gather "
+                            "with no L1 reuse"},
                 "t_probe_us": None if probe_ms is None else 1e3 * float(probe_ms.mean(axis=0)[dom]),
                 "step_aggregate": {"achieved": step_gbs, "frac": step_gbs / hbm,
                                    "what": "compulsory bytes of the whole step / the timed step (1 stream)"},
@@ -923,7 +971,7 @@ def run_escs(args):
                                               "(not in value)"}
         if world == 1 and not args.no_compare:
             summ, rows, best_algs = compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm,
-                                                      with_csr=packed)
+                                                      with_csr=packed, l2_gbs=l2_gbs)
             result["baselines"] = summ
             result["cases_columns"] = list(CASE_COLUMNS)
             result["cases"] = [[r[c] if not isinstance(r[c], float) else round(r[c], 4) for c in CASE_COLUMNS]

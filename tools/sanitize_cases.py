@@ -1,7 +1,8 @@
 """Small escs_spmm cases for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): UFi 1 and 4, vector and scalar lane maps, split and
 heavy panels, empty panels, ragged last panel, long UFi > 1 items (operand
-pipeline), pre-packed values, a grouped launch, the scatter epilogue.  Exits
+pipeline), the packed record walk at every UFi with split and heavy panels,
+a grouped launch, the scatter epilogue.  Exits
 non-zero on a mismatch.
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
@@ -58,6 +59,21 @@ def main():
                         oracle.spmm(W.m, W.k, W.rowptr, W.colidx, Ad.vals, B))
     print("packed", "ok" if ok else "MISMATCH", flush=True)
     bad += not ok
+    # the packed record walk: every UFi (1-4, 6, 8), split and heavy panels
+    # (CTA-parallel workspace combine, named barriers), tails, narrow B
+    for A, n, prm in ((A0, 128, dict(T=7, cta_warps=3)), (P, 64, dict(T=8, cta_warps=4)),
+                      (W, 128, dict(T=300, cta_warps=4)), (P, 32, dict(T=16, cta_warps=2))):
+        for ufi in (1, 2, 3, 4, 6, 8):
+            Ad, B = synth.dyadic_twin(A, n, 11)
+            pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, ufi=ufi, packed=1, **prm)
+            pk = escs.escs_pack(pl, torch.from_numpy(Ad.vals).cuda())
+            C = torch.empty(A.m, n, device="cuda")
+            escs.escs_spmm_packed(pl, pk, torch.from_numpy(B).cuda(), C)
+            torch.cuda.synchronize()
+            ok = np.array_equal(C.cpu().numpy().astype(np.float64),
+                                oracle.spmm(A.m, A.k, A.rowptr, A.colidx, Ad.vals, B))
+            print("records", n, ufi, prm, "ok" if ok else "MISMATCH", flush=True)
+            bad += not ok
     # grouped launch: mixed tile widths (idle warps), heavy panels, a UFi-4 single
     probs = [(A0, 64, dict(ufi=1, T=7, cta_warps=3)), (P, 64, dict(ufi=1, T=16, cta_warps=2)),
              (A0, 64, dict(ufi=1, T=9, cta_warps=5)), (W, 64, dict(ufi=4, T=300, cta_warps=4)),
