@@ -275,10 +275,13 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         if (ep->tile_order) p.tile_order = ep->tile_order;
         if (ep->nthreads) p.nthreads = ep->nthreads;
     }
-    if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > 16)) ||
+    // CTA tile width: up to 16 warps (512 threads, the CSR walk's launch
+    // bounds); up to 28 for the record walk (72 registers x 28 x 32 <= 64K)
+    const int max_warps = p.packed ? 28 : 16;
+    if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > max_warps)) ||
         p.variant < 1 || p.variant > 2 || p.tile_order < 0 || p.tile_order > 2 ||
         !(p.colf == 0 || p.colf == 4 || p.colf == 8 || p.colf == 16)) {
-        fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16, "
+        fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16 (1..28 packed), "
                            "variant 1..2, colf 0/4/8/16, tile_order 0..2)");
         return nullptr;
     }

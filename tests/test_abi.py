@@ -132,3 +132,28 @@ def test_group_arg_errors_without_gpu():
     assert lib.escs_spmm_group(2, None, None, None, None, None) == escs.ESCS_ERR_ARG
     code, msg = escs.escs_last_error()
     assert code == escs.ESCS_ERR_ARG and "NULL" in msg
+
+
+def test_packed_params_host_only():
+    """escs_params.packed: 0/1 accepted (else ESCS_ERR_ARG); the plan reports it
+    and the size of escs_pack's record stream (G records of 2/4/8/12 words by
+    UFi, include/escs.h); tile widths up to 28 warps for the record walk, 16
+    otherwise; host-only plans at UFi 6 and 8 are the canonical plans of the
+    oracle partitioner."""
+    import oracle
+    A = synth.magnitude_pruned(97, 300, 0.8, 5)
+    for bad in ({"packed": 2}, {"packed": -1}, {"cta_warps": 29, "packed": 1}, {"cta_warps": 17}):
+        with pytest.raises(escs.EscsError) as e:
+            escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, host_only=1, **bad)
+        assert e.value.code == escs.ESCS_ERR_ARG
+    words = {1: 2, 2: 4, 3: 4, 4: 8, 6: 8, 8: 12}
+    for h, rw in words.items():
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, ufi=h, T=24, packed=1,
+                               cta_warps=28, host_only=1)
+        info = pl.info
+        assert info["packed"] == 1 and info["h"] == h and info["cta_warps"] == 28
+        assert info["packed_words"] == rw * info["G"]
+        ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, h, 24, bCols=64)
+        got = pl.export()
+        for n in oracle.PLAN_ARRAYS:
+            assert np.array_equal(got[n], ref[n]), (h, n)
