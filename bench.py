@@ -359,7 +359,7 @@ def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None):
     return out
 
 
-CASE_COLUMNS = ("case", "ufi", "t_escs_us", "t_escs_csr_us", "t_cusparse_us", "t_cublas_us",
+CASE_COLUMNS = ("case", "ufi", "walk", "t_escs_us", "t_escs_csr_us", "t_cusparse_us", "t_cublas_us",
                 "t_cublas_tf32_us", "gflops", "eff_GBps", "pct_hbm", "t_hbm_us", "t_fma_us",
                 "t_l1_us", "t_l2_us", "t_probe_us", "probe_frac", "attainable_frac", "l2_gather_frac", "binding")
 
@@ -389,8 +389,10 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         d = dev[p.name]
         st = {}
         t_escs = graph_time(torch, lambda: d["run"](stream), stream, reps=20, stats=st)
+        # the CSR-value walk on the same plan (a staged plan's canonical items
+        # are one per panel, not a tuned CSR-walk plan: not timed)
         t_csr = (graph_time(torch, lambda: escs.escs_spmm(d["plan"], d["vals"], d["B"], d["C"], stream), stream)
-                 if with_csr else None)
+                 if with_csr and not d["plan"].info["staged"] else None)
         t_probe = None
         if d["probe"] is not None:
             try:
@@ -429,7 +431,7 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         bounds = {"hbm": rb["t_hbm_us"], "fma": rb["t_fma_us"], "l1": rb["t_l1_us"]}
         binding = max(bounds, key=bounds.get)
         gbps = rb["bytes_comp"] / (t_us * 1e-6) / 1e9
-        rows.append({"case": p.name, "ufi": inf["h"], "t_escs_us": t_us,
+        rows.append({"case": p.name, "ufi": inf["h"], "walk": "staged" if inf["staged"] else "gather", "t_escs_us": t_us,
                      "t_escs_us_min": 1e3 * st["min"], "t_escs_us_p90": 1e3 * st["p90"],
                      "t_escs_csr_us": None if t_csr is None else 1e3 * t_csr,
                      "t_cusparse_us": None if best is None else 1e3 * best, "cusparse_alg": best_alg,
@@ -441,7 +443,8 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
                      "probe_frac": (1e3 * t_probe / t_us) if t_probe else None,
                      "attainable_frac": bounds[binding] / t_us, "binding": binding,
                      "t_l2_us": rb.get("t_l2_us"), "l2_gather_frac": (rb["t_l2_us"] / t_us) if "t_l2_us" in rb else None,
-                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G")}})
+                     "plan": {k: inf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "n_tiles", "n_heavy", "G",
+                                                  "staged", "st_ctas", "st_warps", "st_npw", "st_nsplit")}})
     bl.bl_cublas_destroy(cub)
     sel = lambda key: [r[key] for r in rows]
     out = {
@@ -450,8 +453,8 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         "geomean_speedup_vs_cusparse": geomean([r["t_cusparse_us"] / r["t_escs_us"] for r in rows if r["t_cusparse_us"]]),
         "geomean_speedup_vs_cublas": geomean([r["t_cublas_us"] / r["t_escs_us"] for r in rows]),
         "geomean_speedup_vs_cublas_tf32": geomean([r["t_cublas_tf32_us"] / r["t_escs_us"] for r in rows]),
-        "geomean_speedup_vs_csr_walk": (geomean([r["t_escs_csr_us"] / r["t_escs_us"] for r in rows])
-                                        if with_csr else None),
+        "geomean_speedup_vs_csr_walk": (geomean([r["t_escs_csr_us"] / r["t_escs_us"] for r in rows
+                                                 if r["t_escs_csr_us"]]) if with_csr else None),
         "pct_faster_than_cusparse": 100.0 * np.mean([r["t_cusparse_us"] is not None and r["t_escs_us"] < r["t_cusparse_us"] for r in rows]),
         "pct_faster_than_cublas": 100.0 * np.mean([r["t_escs_us"] < r["t_cublas_us"] for r in rows]),
         "median_attainable_frac": float(np.median(sel("attainable_frac"))),
@@ -591,7 +594,8 @@ def run_escs(args):
             d["packed"] = escs.escs_pack(pl, vals)
             d["run"] = (lambda d: lambda st, C=None: escs.escs_spmm_packed(
                 d["plan"], d["packed"], d["B"], d["C"] if C is None else C, st))(d)
-            sink = torch.empty(max(1, info["n_tiles"] * 32 * info["cta_warps"]), device=device)
+            sink = torch.empty(max(1, info["n_tiles"] * 32 * info["cta_warps"], info["st_ctas"] * 32 * info["st_warps"]),
+                               device=device)
             d["probe"] = (lambda d, sink: lambda st: escs.escs_gather_probe_packed(
                 d["plan"], d["packed"], d["B"], sink, st))(d, sink)
         else:
@@ -646,9 +650,27 @@ def run_escs(args):
     barrier()
     ev = lambda: torch.cuda.Event(enable_timing=True)
     sleep_cycles = int(2e6 + 4e4 * nprob)
+    # the step as one CUDA graph (the layer sequence of an inference step is
+    # fixed: captured once, replayed per step -- no per-launch host work); the
+    # L2 flush stays outside the graph, before every replay
+    graph = None
+    if not args.eager:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        for _ in range(max(1, args.warmup)):
+            graph.replay()
+        barrier()
+
+    def timed_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
 
     # ---- timed: K steps, L2 flushed before each, step events only (value)
     starts, ends = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+    eager_ms = None
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.nvtx.range_push("bench_timed")   # ncu --nvtx-include bench_timed/
@@ -656,10 +678,20 @@ def run_escs(args):
             flush.zero_()
             torch.cuda._sleep(sleep_cycles)
             starts[s].record(stream)
-            step()
+            timed_step()
             ends[s].record(stream)
         torch.cuda.nvtx.range_pop()
         barrier()
+        if graph is not None:   # the same step launched eagerly (context: launch overhead)
+            e0, e1 = [ev() for _ in range(args.steps)], [ev() for _ in range(args.steps)]
+            for s in range(args.steps):
+                flush.zero_()
+                torch.cuda._sleep(sleep_cycles)
+                e0[s].record(stream)
+                step()
+                e1[s].record(stream)
+            barrier()
+            eager_ms = sum(a.elapsed_time(b) for a, b in zip(e0, e1))
         # ---- the same steps with per-launch events (each kernel's duration,
         # the dominant kernel's roofline; one stream, so each kernel is alone)
         pl_ev = [[[ev(), ev()] for _ in range(nprob)] for _ in range(args.steps)]
@@ -882,6 +914,8 @@ def run_escs(args):
         ufi_mix = {}
         for inf in infos:
             ufi_mix[str(inf["h"])] = ufi_mix.get(str(inf["h"]), 0) + 1
+        n_staged = sum(1 for inf in infos if inf["staged"])
+        launches_per_step = sum(inf["st_launches"] if inf["staged"] else 1 for inf in infos)
         step_gbs = bytes_all * K / (total_ms * 1e-3) / 1e9
         dinf = infos[dom]
         result = {
@@ -890,6 +924,11 @@ def run_escs(args):
             "scaling": "weak" if (world > 1 and mode == "problems") else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "problems": len(problems), "sharding": sharding, "streams": 1,
+                       "launch": ("the step captured once as a CUDA graph and replayed per step (L2 flush outside "
+                                  "the graph)" if graph is not None else "eager launches (--eager)"),
+                       "eager_step": None if eager_ms is None else {
+                           "ms_per_step": eager_ms / K, "value": flops_all * K / (eager_ms * 1e-3) / 1e9,
+                           "what": "the same step launched eagerly, one launch per layer (context)"},
                        "l2": ("flushed before every step (256 MiB write); each problem touched once per step"
                               if not args.hot_l2 else "NOT flushed (--hot-l2 diagnostic, not a bench value)"),
                        "path": ("escs_spmm_packed: the packed record walk on escs_pack's stream (the paper's data "
@@ -902,11 +941,18 @@ def run_escs(args):
                        "ufi_forced": args.ufi or None,
                        "ufi_mix": ufi_mix,
                        "pdl": bool(dinf["pdl"]),
-                       "plan": {k: dinf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant", "n_tiles", "n_heavy", "pdl", "packed")}},
+                       "walks": {"staged": n_staged, "gather": len(infos) - n_staged,
+                                 "what": "staged: B rows of the CTA's k-range in shared memory (TMA bulk copies, "
+                                         "staged_kernel.cuh); gather: B rows gathered from L2 (esc_kernel.cuh record walk); "
+                                         "the plan-time tuner picks per layer"},
+                       "plan": {k: dinf[k] for k in ("h", "T", "cta_warps", "ufk", "colf", "variant", "n_tiles", "n_heavy", "pdl", "packed",
+                                                     "staged", "st_ctas", "st_warps", "st_npw", "st_nsplit", "st_kb",
+                                                     "st_smem_bytes", "st_launches")}},
             "roofline": {
                 "bound": "hbm", "achieved": dom_gbs, "peak": hbm, "unit": "GB/s", "frac": dom_gbs / hbm,
                 "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": f"{'esc_rec_kernel' if dinf['packed'] else 'esc_spmm_kernel'} on the dominant layer {pd.name}",
+                "kernel": f"{'esc_staged_kernel' if dinf['staged'] else 'esc_rec_kernel' if dinf['packed'] else 'esc_spmm_kernel'} "
+                          f"on the dominant layer {pd.name}",
                 "achieved_how": ("compulsory bytes (8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols, SURVEY 8(d)) of the "
                                  "dominant layer / its mean launch duration (CUDA events around each launch on the "
                                  "launching stream, L2 flushed before every step, launches in order on one stream)"),
@@ -934,7 +980,7 @@ def run_escs(args):
                                    "names": [p.name for p, _ in shard_problems],
                                    "us": [round(1e3 * float(x), 3) for x in per_prob],
                                    "ufi": [inf["h"] for inf in infos]},
-            "gpu_launches": nprob * K,
+            "gpu_launches": launches_per_step * K,
             "clocks": clocks,
             "e2e": {"value": flops_all * K / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -1008,6 +1054,8 @@ def main(argv=None):
     ap.add_argument("--streams", type=int, default=16,
                     help="also time the suite with its layers on this many streams (context figure)")
     ap.add_argument("--cases-out", default=None)
+    ap.add_argument("--eager", action="store_true",
+                    help="time the step as eager launches (default: one CUDA-graph replay per step)")
     ap.add_argument("--csr", action="store_true",
                     help="time escs_spmm on the CSR values (the CSR-value walk) instead of the packed record walk")
     ap.add_argument("--ufi", type=int, default=0,

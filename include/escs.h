@@ -248,6 +248,24 @@ typedef struct {
                              the tuner also searches UFi in 1..4
                              unless ufi is given.  0: escs_spmm (CSR values).
                              Either way any call works on the plan.           */
+    int32_t staged;       /* the packed walk's B-row source: 0 = auto (the
+                             autotuner times both walks when it runs; the L2
+                             gather walk otherwise), 1 = gather B rows from
+                             L2 (esc_kernel.cuh record walk), 2 = staged: a
+                             CTA owns a row block (st_warps x st_npw panels)
+                             and one of st_nsplit column ranges of A; TMA bulk
+                             copies bring that range's B rows and the CTA's
+                             records into shared memory and every B row is
+                             read there (staged_kernel.cuh); with st_nsplit >
+                             1 a second launch sums the ranges' partials in
+                             range order.  Staged plans need packed = 1 and
+                             bCols 32, 64 or 128.                            */
+    int32_t st_warps;     /* staged: warps per CTA (1..16), 0 = auto           */
+    int32_t st_npw;       /* staged: panels per warp (1, 2, 4), 0 = auto        */
+    int32_t st_nsplit;    /* staged: column ranges per row block, 0 = auto (fit
+                             227 KB of shared memory, ~1 CTA per SM)          */
+    int32_t st_kb;        /* staged: columns per pipeline stage (one mbarrier
+                             each, <= 16 stages per CTA), 0 = auto             */
     int32_t reserved[1];  /* must be zero                                        */
 } escs_params;
 
@@ -294,6 +312,11 @@ typedef struct {
     int32_t pdl;            /* 1 if launches carry programmatic dependent launch    */
     int32_t packed;         /* 1 if planned (and tuned) for escs_spmm_packed         */
     int64_t packed_words;   /* size of escs_pack's record stream, in 32-bit words   */
+    int32_t staged;         /* 1 if escs_spmm_packed runs the staged walk          */
+    int32_t st_ctas;        /* staged: CTAs of the walk launch (row blocks x ranges) */
+    int32_t st_warps, st_npw, st_nsplit, st_kb;
+    int32_t st_smem_bytes;  /* staged: dynamic shared memory per CTA               */
+    int32_t st_launches;    /* staged: kernel launches per escs_spmm_packed (1, 2)  */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);
@@ -316,6 +339,25 @@ int escs_gather_probe(escs_plan_t plan, const float *B, float *sink, void *strea
 int escs_gather_probe_packed(escs_plan_t plan, const float *packed, const float *B, float *sink,
                              void *stream);
 
+/*
+ * escs_staged_export -- the staged walk's schedule (host copies owned by the
+ * plan, valid until escs_free; plans built with staged = 2, host-only plans
+ * included).  It is derived from the canonical plan: CTA c = (row block rb,
+ * column range sp) owns panels [rb*nslot, (rb+1)*nslot) (nslot = st_warps x
+ * st_npw) and columns [sp*k/nsplit, (sp+1)*k/nsplit), cut into stages of
+ * st_kb columns; record r of the stream escs_pack writes for the plan is the
+ * canonical gcol src[r] (-1: padding), stored by (CTA, stage, slot) and, in a
+ * slot, in canonical order.
+ *   cta[4c..]    rb, sp, first stage, stage count
+ *   stage[4s..]  first column, end column, first record, records (padded)
+ *   hdr[hs*s+j]  record offset (from the CTA's first record) of slot j's
+ *                records in stage s; hdr[hs*s + nslot] = the stage's end
+ */
+typedef struct escs_staged_view {
+    int32_t n_cta, n_stage, n_rec, hs, nslot, max_k, max_rec, max_stages;
+    const int32_t *cta, *stage, *hdr, *src;
+} escs_staged_view;
+int escs_staged_export(escs_plan_t plan, escs_staged_view *out);
 /* Library version string ("escs <ver> sm_100a"). */
 const char *escs_version(void);
 

@@ -4,8 +4,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -68,6 +70,11 @@ void apply_env(escs::Params& p, bool& set_warps) {
             else if (k == "colf") p.colf = v;
             else if (k == "order") p.tile_order = v;
             else if (k == "packed") p.packed = v;
+            else if (k == "staged") p.staged = v;
+            else if (k == "st_warps") p.st_warps = v;
+            else if (k == "st_npw") p.st_npw = v;
+            else if (k == "st_nsplit") p.st_nsplit = v;
+            else if (k == "st_kb") p.st_kb = v;
         }
         i = j + 1;
     }
@@ -131,6 +138,38 @@ size_t add_region(size_t& off, size_t count) {
         }                                                                              \
     } while (0)
 
+// Shared memory a staged CTA may use: the sm_100 opt-in maximum (227 KB)
+// less the kernel's static mbarriers and a margin.
+constexpr size_t kStSmemCap = 227 * 1024 - 8 * 1024 - 512;   // static: mbarriers + combine buffer
+
+// Auto tile of the staged walk: 16 warps x 1 panel per CTA (fewer when the
+// matrix has fewer panels), column ranges so that about one CTA per SM runs
+// (the B range plus the records fill most of the 227 KB), stages of ~16 KB of
+// B rows (at most 16).  build_staged then checks the budget; the caller
+// raises nsplit while it does not fit.
+void auto_staged(escs::Params& p, const escs::PlanHost& ph, int bcols, int n_sm) {
+    const int64_t nP = ph.header[7], k = ph.header[2], G = ph.header[9];
+    if (!p.st_npw) p.st_npw = 1;
+    if (!p.st_warps) p.st_warps = (int)std::max<int64_t>(1, std::min<int64_t>(16, (nP + p.st_npw - 1) / p.st_npw));
+    const int64_t nslot = (int64_t)p.st_warps * p.st_npw;
+    const int64_t n_rb = (nP + nslot - 1) / nslot;
+    if (!p.st_nsplit) {
+        int64_t ns = std::max<int64_t>(1, n_sm / n_rb);   // at most one wave of CTAs
+        const int rw = escs::rec_words(ph.header[5]);
+        for (;; ns++) {
+            const double wd = std::ceil((double)k / ns);
+            const double rec = 1.25 * (double)G / (double)(n_rb * ns) + 64;
+            if ((wd * bcols + rec * rw) * 4.0 + 16 * 4 * 20 <= (double)kStSmemCap || ns >= k) break;
+        }
+        p.st_nsplit = (int)std::min<int64_t>(ns, k);
+    }
+    if (!p.st_kb) {
+        const int64_t wd = (k + p.st_nsplit - 1) / p.st_nsplit;
+        const int64_t kb = std::max<int64_t>(8, 16384 / (4 * bcols));
+        p.st_kb = (int)std::max<int64_t>(kb, (wd + 15) / 16);
+    }
+}
+
 bool upload(escs_plan_impl* P) {
     auto& ph = P->host;
     auto& dp = P->dev;
@@ -181,6 +220,15 @@ bool upload(escs_plan_impl* P) {
     const size_t o_cnt = add_region<int32_t>(off, ph.n_heavy);
     const size_t ws_elems = (size_t)ph.n_heavy_tiles * h * n;
     const size_t o_ws = add_region<float>(off, ws_elems);
+    const auto& st = ph.st;
+    const size_t o_stc = add_region<int32_t>(off, st.cta.size());
+    const size_t o_sts = add_region<int32_t>(off, st.stage.size());
+    const size_t o_sth = add_region<int32_t>(off, st.hdr.size());
+    const size_t o_str = add_region<int32_t>(off, st.src.size());
+    const size_t st_ws = (st.n_cta && st.nsplit > 1) ? (size_t)st.nsplit * ph.header[1] * n : 0;
+    const size_t o_stw = add_region<float>(off, st_ws);
+    const int64_t st_rb = st.n_cta ? st.n_cta / st.nsplit : 0;
+    const size_t o_stk = add_region<int32_t>(off, 2 * st_rb);
     off = std::max<size_t>(off, 256);
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, off);
@@ -191,7 +239,7 @@ bool upload(escs_plan_impl* P) {
     }
     P->dmem = d;
     P->dbytes = off;
-    P->ws_bytes = ws_elems * sizeof(float);
+    P->ws_bytes = (ws_elems + st_ws) * sizeof(float);
     char* b = static_cast<char*>(d);
     auto put = [&](size_t o, const void* src, size_t bytes) -> bool {
         if (!bytes) return true;
@@ -206,6 +254,19 @@ bool upload(escs_plan_impl* P) {
     if (!put(o_tiles, ph.tile_heavy.data(), ph.tile_heavy.size() * 4)) return false;
     if (!put(o_heavy, ph.heavy_info.data(), ph.heavy_info.size() * 4)) return false;
     if (ph.n_heavy) CUDA_TRY(cudaMemset(b + o_cnt, 0, ph.n_heavy * 4));
+    if (!put(o_stc, st.cta.data(), st.cta.size() * 4)) return false;
+    if (!put(o_sts, st.stage.data(), st.stage.size() * 4)) return false;
+    if (!put(o_sth, st.hdr.data(), st.hdr.size() * 4)) return false;
+    if (!put(o_str, st.src.data(), st.src.size() * 4)) return false;
+    if (st.n_cta) {
+        dp.st_cta = reinterpret_cast<const int32_t*>(b + o_stc);
+        dp.st_stage = reinterpret_cast<const int32_t*>(b + o_sts);
+        dp.st_hdr = reinterpret_cast<const int32_t*>(b + o_sth);
+        dp.st_src = reinterpret_cast<const int32_t*>(b + o_str);
+        dp.st_ws = st_ws ? reinterpret_cast<float*>(b + o_stw) : nullptr;
+        dp.st_counters = reinterpret_cast<int32_t*>(b + o_stk);
+        CUDA_TRY(cudaMemset(b + o_stk, 0, 2 * st_rb * 4));
+    }
     dp.gpk = reinterpret_cast<const int32_t*>(b + o_gpk);
     dp.slot = reinterpret_cast<const int32_t*>(b + o_slot);
     dp.vbase = h > 1 ? reinterpret_cast<const int32_t*>(b + o_vb) : nullptr;
@@ -274,6 +335,11 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         if (ep->colf) p.colf = ep->colf;
         if (ep->tile_order) p.tile_order = ep->tile_order;
         if (ep->nthreads) p.nthreads = ep->nthreads;
+        if (ep->staged) p.staged = ep->staged;
+        if (ep->st_warps) p.st_warps = ep->st_warps;
+        if (ep->st_npw) p.st_npw = ep->st_npw;
+        if (ep->st_nsplit) p.st_nsplit = ep->st_nsplit;
+        if (ep->st_kb) p.st_kb = ep->st_kb;
     }
     // CTA tile width: up to 16 warps (512 threads, the CSR walk's launch
     // bounds); up to 28 for the record walk (72 registers x 28 x 32 <= 64K)
@@ -294,6 +360,14 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     }
     if (!host_only && p.h > 4 && k >= (1 << 24)) {
         fail(ESCS_ERR_UNSUPPORTED, "device plans with UFi > 4 need k < 2^24 (packed column words)");
+        return nullptr;
+    }
+    if (p.staged < 0 || p.staged > 2) {
+        fail(ESCS_ERR_ARG, "escs_params.staged must be 0, 1 or 2");
+        return nullptr;
+    }
+    if (p.staged == 2 && !(p.packed && p.variant == 1 && (bCols == 32 || bCols == 64 || bCols == 128))) {
+        fail(ESCS_ERR_UNSUPPORTED, "the staged walk needs packed = 1, the vector lane map and bCols 32, 64 or 128");
         return nullptr;
     }
     if (p.variant != 1) {
@@ -330,6 +404,36 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         else if (to && std::string(to) == "length") p.tile_order = 2;
         if (p.tile_order < 1 || p.tile_order > 2) p.tile_order = auto_tile_order(P->host);
         escs::build_tiles(P->host, p.cta_warps, p.tile_order == 2);
+        if (p.staged == 2) {
+            // lane map of the staged walk: the plan's columns per lane if that
+            // instance exists, else 4
+            const int F = escs::staged_supported(p.h, bCols, p.colf, p.st_npw ? p.st_npw : 1) ? p.colf : 4;
+            if (!escs::staged_supported(p.h, bCols, F, p.st_npw ? p.st_npw : 1)) {
+                delete P;
+                fail(ESCS_ERR_UNSUPPORTED, "no staged kernel for ufi=" + std::to_string(p.h) + " bCols=" +
+                                               std::to_string(bCols) + " npw=" + std::to_string(p.st_npw));
+                return nullptr;
+            }
+            p.colf = F;
+            const bool fixed_split = p.st_nsplit != 0;
+            auto_staged(p, P->host, bCols, host_only ? 148 : sm_count_of_current_device());
+            std::string why;
+            for (int tries = 0; tries < 64; tries++) {
+                why = escs::build_staged(P->host, bCols, p.st_warps, p.st_npw, p.st_nsplit, p.st_kb,
+                                         kStSmemCap, P->host.st);
+                if (why.empty() || fixed_split || p.st_nsplit >= k) break;
+                if (why.find("shared memory") == std::string::npos && why.find("stages") == std::string::npos)
+                    break;
+                p.st_nsplit += std::max(1, p.st_nsplit / 8);   // did not fit: more, narrower ranges
+                const int64_t wd = (k + p.st_nsplit - 1) / p.st_nsplit;
+                p.st_kb = std::max<int>(p.st_kb, (int)((wd + 15) / 16));
+            }
+            if (!why.empty()) {
+                delete P;
+                fail(ESCS_ERR_UNSUPPORTED, "staged walk: " + why);
+                return nullptr;
+            }
+        }
     } catch (const std::bad_alloc&) {
         delete P;
         fail(ESCS_ERR_OOM, "host allocation while planning");
@@ -347,6 +451,14 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
     dp.ufk = p.ufk; dp.colf = p.colf; dp.any_sync = P->host.any_sync;
     dp.G = P->host.header[9];
+    if (P->host.st.n_cta) {
+        const auto& st = P->host.st;
+        dp.st_n_cta = st.n_cta; dp.st_warps = st.warps; dp.st_npw = st.npw; dp.st_nsplit = st.nsplit;
+        dp.st_hs = st.hs; dp.st_max_stages = st.max_stages;
+        dp.st_sb_floats = (st.max_k * bCols + 31) / 32 * 32;   // records start 128-byte aligned
+        dp.st_sr_words = (st.max_rec * st.rw + 3) / 4 * 4;
+        dp.st_n_rec = (int)st.src.size();
+    }
     {
         const char* e = std::getenv("ESCS_PDL");
         dp.pdl = !(e && e[0] == '0');
@@ -357,6 +469,16 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
             return nullptr;
         }
         int e = escs::prepare_kernels(dp);
+        if (!e && dp.st_n_cta) {
+            e = escs::prepare_staged(dp);
+            // the split combine runs in the walk kernel when the whole grid
+            // can be resident at once (cooperative launch); else a second,
+            // tiny kernel sums the partials
+            const char* ec = std::getenv("ESCS_ST_COOP");
+            const int nb = e ? 0 : escs::staged_blocks_per_sm(dp);
+            dp.st_coop = !(ec && ec[0] == '0') && nb > 0 &&
+                         (int64_t)dp.st_n_cta <= (int64_t)nb * sm_count_of_current_device();
+        }
         if (e) {
             fail(ESCS_ERR_CUDA, std::string("kernel attributes: ") +
                                     cudaGetErrorString((cudaError_t)e));
@@ -492,26 +614,91 @@ struct TuneBufs {
 
 constexpr float kFailed = 1e30f;
 
+bool tune_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("ESCS_TUNE_DEBUG");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// One SpMM launch of whichever walk the plan runs (the staged walk for a
+// staged plan's record stream).
+int launch_plan(const escs::DevPlan& dp, const float* v, const float* B, float* C, void* stream, bool vec,
+                bool packed) {
+    if (packed && dp.st_n_cta) return escs::launch_staged(dp, v, B, C, stream);
+    return escs::launch_spmm(dp, v, B, C, stream, vec, packed);
+}
+
 // Latency objective: batches of 16 back-to-back launches queued behind a
 // ~100 us busy-wait (the host enqueues the batch while the GPU spins): GPU
 // time only; min over 3 batches.  A candidate whose launch fails is rejected
 // (time kFailed, CUDA error cleared) -- it must never win by timing no work.
+// Latency objective, graph mode (the default, ESCS_TUNE_GRAPH != 0): the
+// batch of kBatch back-to-back launches is captured once into a CUDA graph
+// and replayed -- the way a fixed layer sequence runs in production (and
+// bench.py's step), launch overhead excluded; min over 3 replays.  Capture
+// failures fall back to eager batches.
+float time_plan_graph(escs_plan_t P, TuneBufs& b, bool packed, const float* v, bool vec) {
+    constexpr int kBatch = 16;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    if (cudaStreamBeginCapture(b.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    bool ok = true;
+    for (int i = 0; i < kBatch; i++) ok = ok && launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
+    const cudaError_t ce = cudaStreamEndCapture(b.stream, &g);
+    if (ce != cudaSuccess || !ok || !g || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        return -1.f;
+    }
+    float best = kFailed;
+    for (int rep = 0; rep < 4 && ok; rep++) {
+        escs::launch_spin(b.stream, 100000);
+        cudaEventRecord(b.e0, b.stream);
+        ok = cudaGraphLaunch(ge, b.stream) == cudaSuccess;
+        cudaEventRecord(b.e1, b.stream);
+        if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            best = kFailed;
+            break;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, b.e0, b.e1);
+        if (rep > 0) best = std::min(best, ms / kBatch);   // the first replay uploads the graph
+    }
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    return best;
+}
+
 float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
     float best = kFailed;
     const bool vec = aligned16(b.B) && aligned16(b.C);
     if (packed && !b.pack_for(P->dev)) return kFailed;
     const float* v = packed ? b.packed : b.vals;
     for (int w = 0; w < 2; w++)
-        if (escs::launch_spmm(P->dev, v, b.B, b.C, b.stream, vec, packed) != 0) {
+        if (launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) != 0) {
             cudaGetLastError();
             return kFailed;
         }
+    static const bool graph = [] {
+        const char* e = std::getenv("ESCS_TUNE_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    if (graph) {
+        const float t = time_plan_graph(P, b, packed, v, vec);
+        if (t >= 0.f) return t;
+    }
     constexpr int kBatch = 16;
     for (int rep = 0; rep < 3; rep++) {
         escs::launch_spin(b.stream, 200000);
         cudaEventRecord(b.e0, b.stream);
         bool ok = true;
-        for (int i = 0; i < kBatch; i++) ok = ok && escs::launch_spmm(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
+        for (int i = 0; i < kBatch; i++) ok = ok && launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
         cudaEventRecord(b.e1, b.stream);
         if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
             cudaGetLastError();
@@ -584,12 +771,75 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b, bool packed) {
 // W, UFk, the bCols coarsening factor and the tile order; every candidate is a
 // complete canonical plan, timed by the chosen objective on the walk it will
 // run (packed: escs_pack then escs_spmm_packed launches).
+// Staged-walk search (escs_params.staged = 2 with autotune, or as the last
+// stage of the packed latency search): UFi x tile (warps x panels per warp)
+// from the B200 sweeps (profiles/r2_notes.md "staged walk"), column ranges
+// automatic (about one co-resident CTA per SM); explicit parameters are not
+// searched.  Returns the fastest, or NULL.
+escs_plan_t make_plan_staged_tuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                                   const int32_t* colidx, int32_t bCols, escs_params q, TuneBufs* shared) {
+    q.autotune = 0;
+    q.staged = 2;
+    q.T = q.T ? q.T : 1 << 20;   // the canonical items are not used by the staged walk: one per panel
+    std::unique_ptr<TuneBufs> own;
+    TuneBufs* bufs = shared;
+    if (!bufs) {
+        own.reset(new TuneBufs(m, k, nnz, bCols, false));
+        if (!own->ok) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+        bufs = own.get();
+    }
+    static const int cand[][3] = {{8, 16, 1}, {4, 16, 2}, {6, 8, 1}, {4, 8, 1}, {3, 16, 1}, {2, 16, 1}};
+    escs_plan_t best = nullptr;
+    float bt = kFailed;
+    for (const auto& x : cand) {
+        escs_params c = q;
+        if (!q.ufi) c.ufi = x[0];
+        if (!q.st_warps) c.st_warps = x[1];
+        if (!q.st_npw) c.st_npw = x[2];
+        bool dup = false;   // explicit parameters collapse candidates
+        for (const auto* y = cand; y != &x; y++)
+            dup = dup || ((q.ufi ? q.ufi : (*y)[0]) == c.ufi && (q.st_warps ? q.st_warps : (*y)[1]) == c.st_warps &&
+                          (q.st_npw ? q.st_npw : (*y)[2]) == c.st_npw);
+        if (dup) continue;
+        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+        if (!P) {
+            if (tune_debug()) std::fprintf(stderr, "escs tune: staged h%d W%d npw%d: %s\n", c.ufi, c.st_warps, c.st_npw, g_msg.c_str());
+            clear_error();
+            continue;
+        }
+        const float t = time_plan(P, *bufs, true);
+        if (tune_debug())
+            std::fprintf(stderr, "escs tune: staged h%d W%d npw%d ns%d ctas %d coop %d: %.2f us\n", c.ufi, c.st_warps,
+                         c.st_npw, P->host.st.nsplit, P->host.st.n_cta, (int)P->dev.st_coop, 1e3f * t);
+        if (t < bt) {
+            if (best) escs_free(best);
+            best = P;
+            bt = t;
+        } else {
+            escs_free(P);
+        }
+    }
+    if (best) {
+        best->autotuned = true;
+        clear_error();
+    } else if (!shared) {
+        return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);   // reports why
+    }
+    return best;
+}
+
 escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                                 const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     escs_params q = ep ? *ep : escs_params{};
     const bool concurrent = q.autotune == 2;
     const bool packed = q.packed != 0;
     q.autotune = 0;
+    // the staged walk is a candidate of the latency objective (its split
+    // combine needs the whole grid resident: not a plan for many streams);
+    // staged = 2 searches only staged plans, 0 both walks
+    const int want_st = (packed && !concurrent) ? q.staged : 1;
+    if (want_st == 2) return make_plan_staged_tuned(m, k, nnz, rowptr, colidx, bCols, q, nullptr);
+    q.staged = 1;
     escs_plan_t first = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
     // Throughput plans launch without programmatic dependent launch: with
     // many streams sharing the SMs, CTAs that start early and wait on the
@@ -759,6 +1009,31 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             best = r1;
         }
     }
+    if (want_st == 0 && best.P->dev.variant == 1 && (bCols == 32 || bCols == 64 || bCols == 128) &&
+        (double)nnz >= 0.15 * (double)m * (double)k && (double)nnz * bCols >= 4.0e7) {
+        // the staged walk where its B-row reuse in shared memory can pay:
+        // dense enough (<= 85% sparsity) and long enough that its fixed costs
+        // (bulk-copy latency before the first stage, the in-kernel combine of
+        // the column ranges) are amortised -- on the B200 suite sweeps it wins
+        // only above ~40M multiply-adds per call (profiles/r2_notes.md); kept
+        // at a 3% margin
+        escs_params c = q;
+        c.staged = 2;
+        escs_plan_t S = make_plan_staged_tuned(m, k, nnz, rowptr, colidx, bCols, c, &bufs);
+        if (S) {
+            const float ts = time_plan(S, bufs, true);
+            if (tune_debug())
+                std::fprintf(stderr, "escs tune: best staged %.2f us vs gather walk %.2f us (h%d)\n", 1e3f * ts,
+                             1e3f * best.t, best.P->params.h);
+            if (ts < 0.97f * best.t) {
+                escs_free(best.P);
+                best = {S, ts};
+            } else {
+                escs_free(S);
+            }
+        }
+        clear_error();
+    }
     best.P->autotuned = true;
     clear_error();
     return best.P;
@@ -811,7 +1086,8 @@ static int spmm_common(escs_plan_t plan, const float* vals, const float* B, floa
                                           "vector-kernel plan (bCols in {4,8,16,32,64,128,256})");
     if (packed && vals && !aligned16(vals))
         return fail(ESCS_ERR_ARG, "the packed record stream must be 16-byte aligned");
-    int e = escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok, packed);
+    int e = (packed && plan->dev.st_n_cta) ? escs::launch_staged(plan->dev, vals, B, C, stream)
+                                           : escs::launch_spmm(plan->dev, vals, B, C, stream, vec_ok, packed);
     if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
     return ESCS_OK;
@@ -916,6 +1192,11 @@ int escs_gather_probe_packed(escs_plan_t plan, const float* packed, const float*
     clear_error();
     if (!plan || plan->host_only || !B || !sink || (!packed && plan->host.header[9] > 0))
         return fail(ESCS_ERR_ARG, "bad probe arguments");
+    if (plan->dev.st_n_cta) {   // the staged walk's probe (sink: st_ctas x st_warps x 32 floats)
+        int e = escs::launch_staged(plan->dev, packed, B, sink, stream, true);
+        if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") + cudaGetErrorString((cudaError_t)e));
+        return ESCS_OK;
+    }
     static const float dummy[4] = {0.f, 0.f, 0.f, 0.f};
     const float* rec = packed ? packed : dummy;   // G = 0: no record is read
     int e = escs::launch_probe(plan->dev, B, sink, stream, aligned16(B), rec);
@@ -986,8 +1267,40 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
         escs::DevPlan d = plan->dev;   // host-only plans: the same formula from the header
         d.h = h.header[5];
         d.G = h.header[9];
+        d.st_n_cta = h.st.n_cta;
+        d.st_n_rec = (int)h.st.src.size();
         o->packed_words = escs::packed_words(d);
     }
+    if (h.st.n_cta) {
+        o->staged = 1;
+        o->st_ctas = h.st.n_cta;
+        o->st_warps = h.st.warps;
+        o->st_npw = h.st.npw;
+        o->st_nsplit = h.st.nsplit;
+        o->st_kb = h.st.kb;
+        o->st_smem_bytes = (int32_t)(plan->host_only ? 0 : escs::staged_smem_bytes(plan->dev));
+        o->st_launches = (h.st.nsplit > 1 && !plan->dev.st_coop) ? 2 : 1;
+    }
+    return ESCS_OK;
+}
+
+int escs_staged_export(escs_plan_t plan, escs_staged_view* out) {
+    clear_error();
+    if (!plan || !out) return fail(ESCS_ERR_ARG, "NULL argument");
+    const auto& st = plan->host.st;
+    if (!st.n_cta) return fail(ESCS_ERR_ARG, "plan has no staged schedule (escs_params.staged = 2)");
+    out->n_cta = st.n_cta;
+    out->n_stage = (int32_t)(st.stage.size() / 4);
+    out->n_rec = (int32_t)st.src.size();
+    out->hs = st.hs;
+    out->nslot = st.nslot;
+    out->max_k = st.max_k;
+    out->max_rec = st.max_rec;
+    out->max_stages = st.max_stages;
+    out->cta = st.cta.data();
+    out->stage = st.stage.data();
+    out->hdr = st.hdr.data();
+    out->src = st.src.data();
     return ESCS_OK;
 }
 

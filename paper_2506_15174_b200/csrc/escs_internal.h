@@ -18,6 +18,23 @@ struct Params {
     int colf = 0;       // B columns per lane of the vector map (bCols coarsening), 0 = default
     int tile_order = 0; // 0 auto, 1 panel order, 2 by longest item
     int nthreads = 0;   // planner threads
+    // staged record walk (staged_kernel.cuh): B rows of a CTA's k-range in
+    // shared memory.  staged: 0 = auto, 1 = off (record walk gathers from L2),
+    // 2 = on; st_*: compute warps per CTA, panels per warp, k-splits per row
+    // block, columns per pipeline stage
+    int staged = 0;
+    int st_warps = 0, st_npw = 0, st_nsplit = 0, st_kb = 0;
+};
+
+// The staged walk's derived schedule (deterministic; a permutation of the
+// canonical record stream cut by row block, k-split, stage and warp slot).
+struct StagedHost {
+    int warps = 0, npw = 0, nsplit = 0, kb = 0, nslot = 0, hs = 0, rw = 0;
+    int n_cta = 0, max_k = 0, max_rec = 0, max_stages = 0;
+    std::vector<int32_t> cta;     // 4 per CTA: rb, split, stage_begin, n_stage
+    std::vector<int32_t> stage;   // 4 per stage: ks, ke, rec_begin, n_rec (padded to 16 bytes)
+    std::vector<int32_t> hdr;     // hs per stage: CTA-relative record offset of each slot, end
+    std::vector<int32_t> src;     // per record: canonical gcol, -1 = padding
 };
 
 // Host plan: the canonical arrays (P1-P8) plus the device-only
@@ -35,6 +52,7 @@ struct PlanHost {
     int n_tiles = 0, n_heavy = 0, n_heavy_tiles = 0, n_split_items = 0;
     bool any_sync = false;
     double plan_seconds = 0.0;
+    StagedHost st;                    // empty unless the plan runs the staged walk
 };
 
 // Validate the CSR.  Returns "" when valid, else a message.
@@ -49,6 +67,14 @@ void build_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
 // fixes UFi, packed selects the table of the record walk.
 Params choose_params(int64_t m, int64_t k, int64_t nnz, int32_t bcols, int n_sm, int h_req = 0,
                      bool packed = false);
+
+// Build the staged walk's schedule from the canonical plan: row blocks of
+// warps x npw panels, nsplit even column splits, stages of kb columns, record
+// words rw per record.  Returns "" or why the configuration does not fit
+// (shared-memory budget smem_cap bytes, at most kStMaxStages stages).
+std::string build_staged(const PlanHost& ph, int bcols, int warps, int npw, int nsplit, int kb,
+                         size_t smem_cap, StagedHost& st);
+int rec_words(int h);   // record stride in 32-bit words (esc_kernel.cuh RecFmt<h>::W)
 
 // Pick cta_warps from the item distribution and build the tile schedule.
 void build_tiles(PlanHost& ph, int cta_warps, bool by_length = true);
@@ -68,6 +94,16 @@ struct DevPlan {
     int G = 0;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
+    // staged walk (st_n_cta > 0): schedule arrays and the split workspace
+    const int32_t* st_cta = nullptr;
+    const int32_t* st_stage = nullptr;
+    const int32_t* st_hdr = nullptr;
+    const int32_t* st_src = nullptr;
+    float* st_ws = nullptr;             // float[nsplit * m * bcols] when nsplit > 1
+    int32_t* st_counters = nullptr;     // 2 per row block (in-kernel split combine)
+    bool st_coop = false;               // grid co-resident: combine in the walk kernel
+    int st_n_cta = 0, st_warps = 0, st_npw = 0, st_nsplit = 0, st_hs = 0, st_max_stages = 0;
+    int st_sb_floats = 0, st_sr_words = 0, st_n_rec = 0;
 };
 
 // Launch the ESC SpMM kernel (one launch).  packed: `vals` is the record
@@ -82,6 +118,14 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
 // escs_pack: the record stream (packed_words(dp) int32 words).
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream);
 int64_t packed_words(const DevPlan& dp);
+// The staged walk: kernel instance exists?  Launch (1 or 2 kernels), shared
+// memory per CTA, kernel attributes.
+bool staged_supported(int h, int bcols, int colf, int npw);
+int launch_staged(const DevPlan& dp, const float* rec, const float* B, float* C, void* stream,
+                  bool probe = false);
+size_t staged_smem_bytes(const DevPlan& dp);
+int prepare_staged(const DevPlan& dp);
+int staged_blocks_per_sm(const DevPlan& dp);
 // Launch the gather probe (same walk, loads only); packed != NULL: the record walk.
 int launch_probe(const DevPlan& dp, const float* B, float* sink, void* stream, bool vec_ok,
                  const float* packed = nullptr);

@@ -20,18 +20,27 @@ namespace kern {
 // writes the gcol's packed word and its pattern rows' values by row, taking
 // the p = popcount(mask) values from slots vbase[j] .. vbase[j] + p - 1
 // (Reading R1: a gcol's values are contiguous in slot order, rows ascending).
+// src != NULL (a staged plan): record q of the output is canonical gcol
+// src[q] (-1: padding, written as zeros).
 template <int H>
 __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict__ gpk,
                                                            const int* __restrict__ slot,
                                                            const int* __restrict__ vbase,
                                                            const float* __restrict__ vals,
+                                                           const int* __restrict__ src,
                                                            int* __restrict__ out, int G) {
     constexpr int RW = RecFmt<H>::W;
     grid_dep_wait();
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < G; j += gridDim.x * blockDim.x) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < G; q += gridDim.x * blockDim.x) {
+        const int j = src ? src[q] : q;
+        if (j < 0) {
+#pragma unroll
+            for (int v = 0; v < RW; v++) out[(size_t)q * RW + v] = 0;
+            continue;
+        }
         const int pk = gpk[j];   // the plan's word: col | mask << RecFmt<H>::Shift
         if constexpr (H == 1) {
-            *reinterpret_cast<int2*>(out + (size_t)j * 2) =
+            *reinterpret_cast<int2*>(out + (size_t)q * 2) =
                 make_int2(pk & RecFmt<1>::ColMask, __float_as_int(vals[j]));
         } else {
             int w[RW];
@@ -43,7 +52,7 @@ __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict
 #pragma unroll
             for (int r = 0; r < H; r++)
                 if ((mk >> r) & 1u) w[1 + r] = __float_as_int(vals[slot[s++]]);
-            int4* o = reinterpret_cast<int4*>(out + (size_t)j * RW);
+            int4* o = reinterpret_cast<int4*>(out + (size_t)q * RW);
 #pragma unroll
             for (int v = 0; v < RW / 4; v++) o[v] = make_int4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
         }
@@ -205,22 +214,26 @@ int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed) {
 
 int64_t packed_words(const DevPlan& dp) {
     const int rw = dp.h == 1 ? 2 : (dp.h <= 3 ? 4 : (dp.h <= 7 ? 8 : 12));   // kern::RecFmt<h>::W
-    return (int64_t)dp.G * rw;
+    return (int64_t)(dp.st_n_cta ? dp.st_n_rec : dp.G) * rw;
 }
 
+// The record stream: canonical gcol order, or -- for a staged plan -- the
+// staged schedule's order (record q = canonical gcol st_src[q]).
 int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* stream) {
-    if (dp.G == 0) return 0;
+    const int n = dp.st_n_cta ? dp.st_n_rec : dp.G;
+    if (n == 0) return 0;
+    const int* src = dp.st_n_cta ? dp.st_src : nullptr;
     const int threads = 256;
-    const int blocks = (int)std::min<long>(((long)dp.G + threads - 1) / threads, 148L * 16);
+    const int blocks = (int)std::min<long>(((long)n + threads - 1) / threads, 148L * 16);
     int* out = reinterpret_cast<int*>(packed);
     cudaStream_t st = (cudaStream_t)stream;
     switch (dp.h) {
-        case 1: kern::esc_pack_rec_kernel<1><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
-        case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
-        case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
-        case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
-        case 6: kern::esc_pack_rec_kernel<6><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
-        case 8: kern::esc_pack_rec_kernel<8><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, out, dp.G); break;
+        case 1: kern::esc_pack_rec_kernel<1><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 6: kern::esc_pack_rec_kernel<6><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 8: kern::esc_pack_rec_kernel<8><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
         default: return (int)cudaErrorInvalidConfiguration;
     }
     return (int)cudaGetLastError();

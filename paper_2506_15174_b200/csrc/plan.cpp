@@ -332,6 +332,113 @@ void build_tiles(PlanHost& ph, int W, bool by_length) {
     ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 
+int rec_words(int h) { return h == 1 ? 2 : (h <= 3 ? 4 : (h <= 7 ? 8 : 12)); }
+
+// The staged walk's schedule.  Row block rb = panels [rb*nslot, (rb+1)*nslot)
+// (nslot = warps x npw; warp w owns slots w*npw .. w*npw + npw - 1), split sp
+// = columns [sp*k/nsplit, (sp+1)*k/nsplit), stage = kb columns of a split.
+// CTA (rb, sp) = rb*nsplit + sp.  Its records: for each stage, for each slot,
+// the slot panel's gcols whose column lies in the stage, in canonical gcol
+// order (a stable counting sort by (stage, slot) of the panels' streams), each
+// stage padded to 16 bytes.  Every canonical gcol lands in exactly one record
+// (tests/test_staged.py checks the permutation against the exported plan).
+std::string build_staged(const PlanHost& ph, int bcols, int warps, int npw, int nsplit, int kb,
+                         size_t smem_cap, StagedHost& st) {
+    const int64_t k = ph.header[2], nP = ph.header[7], NG = ph.header[8];
+    const int h = ph.header[5];
+    if (warps < 1 || warps > 16 || npw < 1 || npw > 4 || nsplit < 1 || kb < 1)
+        return "staged parameters out of range (warps 1..16, npw 1..4, nsplit >= 1, kb >= 1)";
+    if (nsplit > k) return "more k-splits than columns";
+    st = StagedHost();
+    st.warps = warps; st.npw = npw; st.nsplit = nsplit; st.kb = kb;
+    st.nslot = warps * npw;
+    st.hs = (st.nslot + 1 + 3) & ~3;
+    st.rw = rec_words(h);
+    const int64_t pad = st.rw >= 4 ? 1 : 16 / (4 * st.rw);   // records per 16 bytes
+    const int64_t nslot = st.nslot;
+    const int64_t n_rb = (nP + nslot - 1) / nslot;
+    if (n_rb * nsplit >= INT32_MAX) return "too many CTAs";
+    auto ks = [&](int64_t sp) { return (sp * k) / nsplit; };
+    int max_st = 0;
+    for (int64_t sp = 0; sp < nsplit; sp++) {
+        const int64_t wd = ks(sp + 1) - ks(sp);
+        max_st = std::max<int>(max_st, (int)((wd + kb - 1) / kb));
+        st.max_k = std::max<int>(st.max_k, (int)wd);
+    }
+    if (max_st > 16) return "more than 16 stages per CTA (raise kb or nsplit)";
+    st.max_stages = max_st;
+    // first group of each panel (groups are ordered by panel)
+    std::vector<int64_t> pg(nP + 1, NG);
+    for (int64_t g = NG - 1; g >= 0; g--) pg[ph.grp_panel[g]] = g;
+    for (int64_t P = nP - 1; P >= 0; P--) pg[P] = std::min(pg[P], pg[P + 1]);
+    const int64_t nkey = (int64_t)nsplit * max_st * nslot;
+    std::vector<int64_t> cnt(nkey + 1), pos(nkey);
+    std::vector<int32_t> keyed;   // gcols of the row block by key
+    int64_t R = 0;                // records emitted (absolute)
+    for (int64_t rb = 0; rb < n_rb; rb++) {
+        std::fill(cnt.begin(), cnt.end(), 0);
+        auto key_of = [&](int64_t j, int32_t col) {
+            const int64_t sp = (((int64_t)col + 1) * nsplit - 1) / k;
+            const int64_t s = (col - ks(sp)) / kb;
+            return (sp * max_st + s) * nslot + j;
+        };
+        for (int64_t j = 0; j < nslot; j++) {
+            const int64_t P = rb * nslot + j;
+            if (P >= nP) break;
+            for (int64_t c = ph.grp_col_ptr[pg[P]]; c < ph.grp_col_ptr[pg[P + 1]]; c++)
+                cnt[key_of(j, ph.gcol[c]) + 1]++;
+        }
+        for (int64_t x = 0; x < nkey; x++) cnt[x + 1] += cnt[x];
+        keyed.assign(cnt[nkey], 0);
+        for (int64_t x = 0; x < nkey; x++) pos[x] = cnt[x];
+        for (int64_t j = 0; j < nslot; j++) {
+            const int64_t P = rb * nslot + j;
+            if (P >= nP) break;
+            for (int64_t c = ph.grp_col_ptr[pg[P]]; c < ph.grp_col_ptr[pg[P + 1]]; c++)
+                keyed[pos[key_of(j, ph.gcol[c])]++] = (int32_t)c;
+        }
+        for (int64_t sp = 0; sp < nsplit; sp++) {
+            const int64_t k0 = ks(sp), k1 = ks(sp + 1);
+            const int nst = (int)((k1 - k0 + kb - 1) / kb);
+            const int64_t rec0 = R;
+            // stage entries and headers at a fixed stride of max_stages per
+            // CTA (zero padding): a CTA finds its stages from blockIdx alone,
+            // so its first loads are independent of each other
+            st.cta.insert(st.cta.end(), {(int32_t)rb, (int32_t)sp, (int32_t)(st.stage.size() / 4), nst});
+            for (int s = 0; s < nst; s++) {
+                const int64_t a = k0 + (int64_t)s * kb, b = std::min<int64_t>(k1, a + kb);
+                const int64_t r0 = R;
+                const size_t hb = st.hdr.size();
+                st.hdr.resize(hb + st.hs, 0);
+                for (int64_t j = 0; j < nslot; j++) {
+                    const int64_t x = (sp * max_st + s) * nslot + j;
+                    st.hdr[hb + j] = (int32_t)(R - rec0);
+                    for (int64_t q = cnt[x]; q < cnt[x + 1]; q++) st.src.push_back(keyed[q]);
+                    R += cnt[x + 1] - cnt[x];
+                }
+                st.hdr[hb + nslot] = (int32_t)(R - rec0);
+                while (R % pad) {
+                    st.src.push_back(-1);
+                    R++;
+                }
+                st.stage.insert(st.stage.end(), {(int32_t)a, (int32_t)b, (int32_t)r0, (int32_t)(R - r0)});
+                if (R >= INT32_MAX) return "staged record stream too large";
+            }
+            for (int s = nst; s < max_st; s++) {
+                st.stage.insert(st.stage.end(), {0, 0, 0, 0});
+                st.hdr.resize(st.hdr.size() + st.hs, 0);
+            }
+            st.max_rec = std::max<int>(st.max_rec, (int)(R - rec0));
+        }
+    }
+    st.n_cta = (int)(st.cta.size() / 4);
+    const size_t need = ((size_t)st.max_k * bcols + (size_t)st.max_rec * st.rw + (size_t)st.max_stages * st.hs) * 4;
+    if (need > smem_cap)
+        return "staged CTA needs " + std::to_string(need) + " bytes of shared memory (cap " +
+               std::to_string(smem_cap) + "): raise nsplit";
+    return "";
+}
+
 // Parameter table (§3.5 Scheduler & Tuner), fitted to the
 // profiling sweeps of tools/tune.py on B200 (profiles/r1_tune_*.json,
 // profiles/r2_notes.md):

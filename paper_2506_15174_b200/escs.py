@@ -23,7 +23,7 @@ PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "s
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
                     "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
                     "escs_pack", "escs_spmm_packed", "escs_spmm_scatter", "escs_spmm_group",
-                    "escs_gather_probe_packed")
+                    "escs_gather_probe_packed", "escs_staged_export")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -37,7 +37,15 @@ class _Params(ctypes.Structure):
                 ("cta_warps", ctypes.c_int32), ("variant", ctypes.c_int32), ("ufk", ctypes.c_int32),
                 ("nthreads", ctypes.c_int32), ("autotune", ctypes.c_int32),
                 ("colf", ctypes.c_int32), ("tile_order", ctypes.c_int32),
-                ("packed", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("packed", ctypes.c_int32), ("staged", ctypes.c_int32), ("st_warps", ctypes.c_int32),
+                ("st_npw", ctypes.c_int32), ("st_nsplit", ctypes.c_int32), ("st_kb", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 1)]
+
+
+class _StagedView(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("n_cta", "n_stage", "n_rec", "hs", "nslot", "max_k",
+                                              "max_rec", "max_stages")] + \
+               [(n, ctypes.POINTER(ctypes.c_int32)) for n in ("cta", "stage", "hdr", "src")]
 
 
 class _View(ctypes.Structure):
@@ -53,7 +61,9 @@ class _Stats(ctypes.Structure):
                [("plan_seconds", ctypes.c_double), ("ctas_per_sm", ctypes.c_int32),
                 ("autotuned", ctypes.c_int32), ("colf", ctypes.c_int32),
                 ("tile_order", ctypes.c_int32), ("pdl", ctypes.c_int32), ("packed", ctypes.c_int32),
-                ("packed_words", ctypes.c_int64)]
+                ("packed_words", ctypes.c_int64)] + \
+               [(n, ctypes.c_int32) for n in ("staged", "st_ctas", "st_warps", "st_npw", "st_nsplit",
+                                              "st_kb", "st_smem_bytes", "st_launches")]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -85,6 +95,8 @@ _lib.escs_plan_export.argtypes = [_vp, ctypes.POINTER(_View)]
 _lib.escs_plan_export.restype = ctypes.c_int
 _lib.escs_plan_info.argtypes = [_vp, ctypes.POINTER(_Stats)]
 _lib.escs_plan_info.restype = ctypes.c_int
+_lib.escs_staged_export.argtypes = [_vp, ctypes.POINTER(_StagedView)]
+_lib.escs_staged_export.restype = ctypes.c_int
 _lib.escs_version.argtypes = []
 _lib.escs_version.restype = ctypes.c_char_p
 
@@ -153,14 +165,18 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
-                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0, packed=0) -> Plan:
+                 variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0, packed=0,
+                 staged=0, st_warps=0, st_npw=0, st_nsplit=0, st_kb=0) -> Plan:
     """escs_plan with explicit escs_params (include/escs.h); 0 = auto for every
     field.  autotune: 1 = latency objective (one stream), 2 = concurrent
     throughput objective (independent SpMMs overlapped on several streams).
-    packed=1: plan (and tune, including UFi) for escs_pack + escs_spmm_packed."""
+    packed=1: plan (and tune, including UFi) for escs_pack + escs_spmm_packed.
+    staged: 0 auto, 1 L2-gather record walk, 2 staged walk (B rows in shared
+    memory); st_*: its tile parameters (0 = auto)."""
     rowptr, colidx = _csr_args(rowptr, colidx)
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
                 int(nthreads), int(autotune), int(colf), int(tile_order), int(packed),
+                int(staged), int(st_warps), int(st_npw), int(st_nsplit), int(st_kb),
                 (ctypes.c_int32 * 1)())
     h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
                           int(bCols), ctypes.byref(p))
@@ -309,6 +325,26 @@ def escs_plan_export(plan: Plan) -> dict:
         cnt = sizes[n]
         ptr = getattr(v, n)
         out[n] = np.ctypeslib.as_array(ptr, shape=(cnt,)).copy() if cnt else np.zeros(0, np.int32)
+    return out
+
+
+def escs_staged_export(plan: Plan) -> dict:
+    """The staged walk's schedule (include/escs.h escs_staged_export) as numpy
+    arrays: cta (n_cta x 4), stage (n_stage x 4), hdr (n_stage x hs), src."""
+    v = _StagedView()
+    if _lib.escs_staged_export(plan.handle, ctypes.byref(v)) != ESCS_OK:
+        _raise_last()
+    out = {n: int(getattr(v, n)) for n in ("n_cta", "n_stage", "n_rec", "hs", "nslot", "max_k",
+                                           "max_rec", "max_stages")}
+
+    def arr(name, cnt, shape):
+        if not cnt:
+            return np.zeros(shape if shape[0] == 0 else (0,), np.int32).reshape(shape)
+        return np.ctypeslib.as_array(getattr(v, name), shape=(cnt,)).copy().reshape(shape)
+    out["cta"] = arr("cta", 4 * out["n_cta"], (out["n_cta"], 4))
+    out["stage"] = arr("stage", 4 * out["n_stage"], (out["n_stage"], 4))
+    out["hdr"] = arr("hdr", out["hs"] * out["n_stage"], (out["n_stage"], out["hs"]))
+    out["src"] = arr("src", out["n_rec"], (out["n_rec"],))
     return out
 
 

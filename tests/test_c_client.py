@@ -42,7 +42,7 @@ def test_struct_layouts_match_binding(tmp_path):
     import ctypes
     from paper_2506_15174_b200 import escs
     structs = {"escs_params": escs._Params, "escs_plan_stats": escs._Stats,
-               "escs_plan_view": escs._View}
+               "escs_plan_view": escs._View, "escs_staged_view": escs._StagedView}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "escs.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--objective", type=int, default=1,
                     help="autotune objective: 1 latency (serial/per-case plans), 2 concurrent "
                          "throughput (the plans bench.py's multi-stream step runs)")
+    ap.add_argument("--staged", default=None,
+                    help="h,warps,npw,nsplit[,kb]: a staged-walk plan with these parameters")
     a = ap.parse_args()
     import torch
     from paper_2506_15174_b200 import escs, synth
@@ -50,14 +52,19 @@ def main():
         world, rank = (int(x) for x in a.shard.split("/"))
         r0, r1 = synth.shard_bounds(A.m, world, rank)
         A = synth.row_block(A, r0, r1)
-    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
-                           autotune=(a.objective if a.autotune and A.nnz <= 8_000_000 else 0),
-                           packed=0 if a.csr else 1, ufi=a.ufi)
+    if a.staged:
+        v = [int(x) for x in a.staged.split(",")] + [0]
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1], packed=1, staged=2,
+                               ufi=v[0], st_warps=v[1], st_npw=v[2], st_nsplit=v[3], st_kb=v[4])
+    else:
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, B.shape[1],
+                               autotune=(a.objective if a.autotune and A.nnz <= 8_000_000 else 0),
+                               packed=0 if a.csr else 1, ufi=a.ufi)
     print(pl.info, flush=True)
     dv, dB = torch.from_numpy(A.vals).cuda(), torch.from_numpy(B).cuda()
     pk = None if a.csr else escs.escs_pack(pl, dv)
     dC = torch.empty(A.m, B.shape[1], device="cuda")
-    sink = torch.empty(pl.info["n_tiles"] * 32 * pl.info["cta_warps"], device="cuda")
+    sink = torch.empty(max(1, pl.info["n_tiles"] * 32 * pl.info["cta_warps"]), device="cuda")
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("profile_reps")      # ncu --nvtx-include profile_reps/
     for i in range(a.reps):
