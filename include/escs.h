@@ -231,6 +231,10 @@ typedef struct {
                              plans that leave SMs to the other streams;
                              such plans launch without programmatic
                              dependent launch).
+                             Candidates are timed as CUDA-graph replays of
+                             back-to-back launches (ESCS_TUNE_GRAPH=0: eager).
+                             The chosen parameters are cached per problem
+                             class (escs_plan_stats.autotuned).
                              Any other value: ESCS_ERR_ARG.                   */
     int32_t colf;         /* B columns per lane of the vector kernel: the bCols
                              coarsening factor (register tile of B columns,
@@ -306,12 +310,17 @@ typedef struct {
     int64_t workspace_bytes;
     double plan_seconds;    /* host enumeration time                              */
     int32_t ctas_per_sm;    /* resident CTAs per SM of the launch (occupancy), 0 host-only */
-    int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing */
+    int32_t autotuned;      /* 1 if the parameters were chosen by plan-time timing,
+                               2 if taken from the process's tuning cache (the
+                               tuned parameters of an earlier matrix with the
+                               same m, k, nnz, bCols and requested parameters;
+                               ESCS_TUNE_CACHE=0 disables the cache)           */
     int32_t colf;           /* B columns per lane of the launch's lane map (0 scalar map) */
     int32_t tile_order;     /* 1 panel order, 2 by item length (resolved)          */
     int32_t pdl;            /* 1 if launches carry programmatic dependent launch    */
     int32_t packed;         /* 1 if planned (and tuned) for escs_spmm_packed         */
-    int64_t packed_words;   /* size of escs_pack's record stream, in 32-bit words   */
+    int64_t packed_words;   /* size of the buffer escs_pack fills, in 32-bit words
+                               (the record stream rounded up to 16 bytes)         */
     int32_t staged;         /* 1 if escs_spmm_packed runs the staged walk          */
     int32_t st_ctas;        /* staged: CTAs of the walk launch (row blocks x ranges) */
     int32_t st_warps, st_npw, st_nsplit, st_kb;

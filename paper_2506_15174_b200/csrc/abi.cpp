@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -23,7 +25,7 @@ struct escs_plan_impl {
     int device = -1;
     void* dmem = nullptr;
     size_t dbytes = 0, ws_bytes = 0;
-    bool autotuned = false;
+    int autotuned = 0;   // 1: tuned at plan time, 2: parameters from the tuning cache
 };
 
 namespace {
@@ -154,7 +156,12 @@ void auto_staged(escs::Params& p, const escs::PlanHost& ph, int bcols, int n_sm)
     const int64_t nslot = (int64_t)p.st_warps * p.st_npw;
     const int64_t n_rb = (nP + nslot - 1) / nslot;
     if (!p.st_nsplit) {
-        int64_t ns = std::max<int64_t>(1, n_sm / n_rb);   // at most one wave of CTAs
+        // at most one wave of CTAs, leaving a few SMs free: a grid of exactly
+        // one CTA per SM waits, launch after launch, for the last SM to drain
+        // the previous kernel while its row blocks' CTAs spin in the combine
+        // (512x4608@70% b128 eager: 148 CTAs 40 us, 144 CTAs 20.6 us;
+        // profiles/r2_notes.md)
+        int64_t ns = std::max<int64_t>(1, std::max(1, n_sm - 4) / n_rb);
         const int rw = escs::rec_words(ph.header[5]);
         for (;; ns++) {
             const double wd = std::ceil((double)k / ns);
@@ -1039,6 +1046,28 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     return best.P;
 }
 
+// Tuning cache (the paper tunes per architecture and bCols; here per
+// problem class): the parameters the tuner chose for (device, m, k, nnz,
+// bCols, requested parameters) are reused for the next matrix of the same
+// class -- the same layer shape pruned to the same density -- which is then
+// planned with them directly (escs_plan_stats.autotuned = 2).  Process-wide,
+// thread-safe; ESCS_TUNE_CACHE=0 disables it.
+struct TuneKey {
+    int64_t m, k, nnz;
+    int32_t bcols, device;
+    escs_params q;
+    bool operator<(const TuneKey& o) const {
+        if (m != o.m) return m < o.m;
+        if (k != o.k) return k < o.k;
+        if (nnz != o.nnz) return nnz < o.nnz;
+        if (bcols != o.bcols) return bcols < o.bcols;
+        if (device != o.device) return device < o.device;
+        return std::memcmp(&q, &o.q, sizeof(q)) < 0;
+    }
+};
+std::mutex g_tune_mu;
+std::map<TuneKey, std::pair<escs_params, bool>> g_tune_cache;   // params, pdl
+
 escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                       const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     const char* env = std::getenv("ESCS_AUTOTUNE");
@@ -1048,7 +1077,60 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
     }
     const bool tune = (ep && ep->autotune) || (env && env[0] == '1');
     if (!tune || (ep && ep->host_only)) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, ep);
-    return make_plan_autotuned(m, k, nnz, rowptr, colidx, bCols, ep);
+    const char* ce = std::getenv("ESCS_TUNE_CACHE");
+    const bool use_cache = !(ce && ce[0] == '0');
+    TuneKey key{m, k, nnz, bCols, -1, ep ? *ep : escs_params{}};
+    key.q.nthreads = 0;
+    if (!key.q.autotune) key.q.autotune = 1;
+    cudaGetDevice(&key.device);
+    if (use_cache) {
+        std::pair<escs_params, bool> hit;
+        bool found = false;
+        {
+            std::lock_guard<std::mutex> lk(g_tune_mu);
+            auto it = g_tune_cache.find(key);
+            if (it != g_tune_cache.end()) {
+                hit = it->second;
+                found = true;
+            }
+        }
+        if (found) {
+            escs_params c = hit.first;
+            c.nthreads = ep ? ep->nthreads : 0;
+            escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+            if (P) {
+                P->dev.pdl = hit.second;
+                P->autotuned = 2;
+                return P;
+            }
+            clear_error();   // fall through: tune this matrix
+        }
+    }
+    escs_plan_t P = make_plan_autotuned(m, k, nnz, rowptr, colidx, bCols, ep);
+    if (P && use_cache && P->autotuned) {
+        escs_params c = key.q;
+        c.autotune = 0;
+        c.ufi = P->params.h;
+        c.T = P->params.T;
+        c.cta_warps = P->params.cta_warps;
+        c.variant = P->params.variant;
+        c.ufk = P->params.ufk;
+        c.colf = P->dev.variant == 1 ? P->params.colf : 0;
+        c.tile_order = P->params.tile_order;
+        c.packed = P->params.packed;
+        if (P->host.st.n_cta) {
+            c.staged = 2;
+            c.st_warps = P->host.st.warps;
+            c.st_npw = P->host.st.npw;
+            c.st_nsplit = P->host.st.nsplit;
+            c.st_kb = P->host.st.kb;
+        } else if (c.packed) {
+            c.staged = 1;
+        }
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        g_tune_cache[key] = {c, P->dev.pdl};
+    }
+    return P;
 }
 
 }  // namespace
@@ -1259,7 +1341,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->packed = plan->params.packed;
     o->ctas_per_sm = plan->host_only ? 0 : escs::blocks_per_sm(plan->dev, plan->dev.variant == 1, false,
                                                                o->packed != 0);
-    o->autotuned = plan->autotuned ? 1 : 0;
+    o->autotuned = plan->autotuned;
     o->colf = plan->dev.variant == 1 ? plan->params.colf : 0;
     o->tile_order = plan->params.tile_order;
     o->pdl = plan->dev.pdl ? 1 : 0;

@@ -57,6 +57,7 @@ struct KParams {
     const float* __restrict__ B;
     float* __restrict__ C;
     int m, n;
+    int k;                             // rows of B (the walk's L2 prefetch of B)
     // fused row-block all-gather (escs_spmm_scatter): every output row is
     // also stored to extra[d] + (row_off + row) * n, d < n_extra -- the peers'
     // C buffers (P2P / NVLink stores through mapped symmetric memory)
@@ -549,6 +550,15 @@ __device__ __forceinline__ void rec_batch(const PP& p, const int* rec, int i, in
     }
 }
 
+// Fire-and-forget bulk prefetch of [q, q + bytes) into L2 (TMA; no
+// completion to wait for).  q 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* q, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(bytes) : "memory");
+}
+
+#ifndef ESC_REC_L2PF
+#define ESC_REC_L2PF 0   // measured: no gain on the cold step, +0.2-0.4 us on the small hot layers
+#endif
 // Walk one item's records [beg, end) (record j = canonical gcol j).
 template <int H, class Map, int U, bool PROBE, class PP>
 __device__ __forceinline__ void walk_rec(const PP& p, int beg, int end, float (&acc)[H][Map::F],
@@ -569,7 +579,30 @@ __device__ __forceinline__ void walk_rec(const PP& p, int beg, int end, float (&
         if (lane < kLines && beg + lane * (128 / (RecFmt<H>::W * 4)) < end)
             asm volatile("prefetch.global.L1 [%0];" ::"l"(rec + (size_t)beg * RecFmt<H>::W + lane * 32));
     }
+#if ESC_REC_L2PF
+    // the item's whole record range into L2 in one bulk request (on a cold L2
+    // the walk's later batches then wait on an L2 hit, not a DRAM round trip)
+    if (lane == 0 && end > beg) {
+        const char* a = reinterpret_cast<const char*>(rec + (size_t)beg * RecFmt<H>::W);
+        const char* a0 = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(15));
+        const char* b1 = reinterpret_cast<const char*>(rec + (size_t)end * RecFmt<H>::W);
+        prefetch_l2_bulk(a0, (uint32_t)(((b1 - a0) + 15) & ~15));
+    }
+#endif
     grid_dep_wait();
+#if ESC_REC_L2PF
+    // this CTA's share of B into L2 (B is caller data: after the wait); every
+    // row is gathered by many warps, most of them on other SMs
+    if (lane == 0 && (threadIdx.x >> 5) == 0 && p.k > 0) {
+        const size_t total = (size_t)p.k * p.n * 4;
+        const size_t chunk = ((total + gridDim.x - 1) / gridDim.x + 255) & ~size_t(255);
+        const size_t off = (size_t)blockIdx.x * chunk;
+        if (off < total) {
+            const size_t len = (total - off < chunk ? total - off : chunk);
+            prefetch_l2_bulk(reinterpret_cast<const char*>(p.B) + off, (uint32_t)((len + 15) & ~size_t(15)));
+        }
+    }
+#endif
     int i = beg;
 #pragma unroll 1
     for (; i + US <= end; i += US)

@@ -105,6 +105,7 @@ kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, 
     p.C = C;
     p.m = dp.m;
     p.n = dp.bcols;
+    p.k = dp.k;
     return p;
 }
 
@@ -214,7 +215,9 @@ int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed) {
 
 int64_t packed_words(const DevPlan& dp) {
     const int rw = dp.h == 1 ? 2 : (dp.h <= 3 ? 4 : (dp.h <= 7 ? 8 : 12));   // kern::RecFmt<h>::W
-    return (int64_t)(dp.st_n_cta ? dp.st_n_rec : dp.G) * rw;
+    // rounded to 16 bytes: bulk copies / prefetches of a range's last record
+    // never reach past the buffer
+    return ((int64_t)(dp.st_n_cta ? dp.st_n_rec : dp.G) * rw + 3) / 4 * 4;
 }
 
 // The record stream: canonical gcol order, or -- for a staged plan -- the

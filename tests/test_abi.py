@@ -152,7 +152,7 @@ def test_packed_params_host_only():
                                cta_warps=28, host_only=1)
         info = pl.info
         assert info["packed"] == 1 and info["h"] == h and info["cta_warps"] == 28
-        assert info["packed_words"] == rw * info["G"]
+        assert info["packed_words"] == (rw * info["G"] + 3) // 4 * 4   # rounded to 16 bytes
         ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, h, 24, bCols=64)
         got = pl.export()
         for n in oracle.PLAN_ARRAYS:

@@ -291,7 +291,7 @@ def test_autotuned_plan_parity(torch_cuda):
     A, B = synth.dyadic_twin(A0, 64, 42)
     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, autotune=1)
     info = pl.info
-    assert info["autotuned"] == 1
+    assert info["autotuned"] in (1, 2)
     got = pl.export()
     ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, info["h"], info["T"], bCols=64)
     for n in oracle.PLAN_ARRAYS:
@@ -313,7 +313,7 @@ def test_throughput_tuned_plan_parity(torch_cuda, shape):
     A, B = synth.dyadic_twin(A0, n, 44)
     C, pl = run_escs(torch_cuda, A, B, autotune=2)
     info = pl.info
-    assert info["autotuned"] == 1
+    assert info["autotuned"] in (1, 2)
     got = pl.export()
     ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, info["h"], info["T"], bCols=n)
     for nm in oracle.PLAN_ARRAYS:
@@ -433,7 +433,7 @@ def test_autotuned_plan_reports_lane_map(torch_cuda):
     p = synth.transformer_suite(bcols=(128,), sparsities=(0.7,))[1]
     A = p.A
     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 128, autotune=1)
-    assert pl.info["autotuned"] == 1 and pl.info["colf"] in (4, 8, 16)
+    assert pl.info["autotuned"] in (1, 2) and pl.info["colf"] in (4, 8, 16)
     C, _ = run_escs(torch_cuda, A, p.B, autotune=1)
     check_tol(A, p.B, C)
 

@@ -86,7 +86,7 @@ def test_records_and_result(torch_cuda, ufi, n, colf):
     C, pl, pk, dv, dB = run_packed(torch, A, B, **kw)
     info = pl.info
     assert info["h"] == ufi and info["colf"] == colf and info["packed"] == 1
-    assert info["packed_words"] == info["G"] * RW[ufi]
+    assert info["packed_words"] == (info["G"] * RW[ufi] + 3) // 4 * 4   # rounded to 16 bytes
     exp = expected_records(pl.export(), A.vals, ufi)
     assert np.array_equal(pk.cpu().numpy()[:len(exp)], exp)
     C_csr = torch.empty(A.m, n, device="cuda")
@@ -138,7 +138,7 @@ def test_packed_autotuned_plan_parity(torch_cuda, shape, autotune):
     A, B = synth.dyadic_twin(A0, n, 75)
     C, pl, pk, dv, dB = run_packed(torch, A, B, autotune=autotune, packed=1)
     info = pl.info
-    assert info["autotuned"] == 1 and info["packed"] == 1
+    assert info["autotuned"] in (1, 2) and info["packed"] == 1
     got = pl.export()
     ref = oracle.partition(A.m, A.k, A.rowptr, A.colidx, info["h"], info["T"], bCols=n)
     for nm in oracle.PLAN_ARRAYS:

@@ -171,3 +171,26 @@ def test_staged_autotuned_suite_layers(torch_cuda):
             escs.escs_spmm_packed(pl, pk, torch_cuda.from_numpy(p.B).cuda(), C)
             torch_cuda.cuda.synchronize()
             check_tol(A, p.B, C.cpu().numpy())
+
+
+def test_tuning_cache_reuses_parameters(torch_cuda, monkeypatch):
+    """A second matrix of the same class (shape, nnz, bCols, request) is planned
+    with the first one's tuned parameters (autotuned = 2), and is exact."""
+    from paper_2506_15174_b200 import escs
+    monkeypatch.delenv("ESCS_TUNE_CACHE", raising=False)
+    A1 = synth.magnitude_pruned(384, 768, 0.8, 501)
+    A2 = synth.magnitude_pruned(384, 768, 0.8, 502)
+    assert A1.nnz == A2.nnz
+    p1 = escs.escs_plan_ex(A1.m, A1.k, A1.nnz, A1.rowptr, A1.colidx, 64, packed=1, autotune=1, tile_order=1)
+    p2 = escs.escs_plan_ex(A2.m, A2.k, A2.nnz, A2.rowptr, A2.colidx, 64, packed=1, autotune=1, tile_order=1)
+    i1, i2 = p1.info, p2.info
+    assert i1["autotuned"] == 1 and i2["autotuned"] == 2
+    for key in ("h", "T", "cta_warps", "ufk", "colf", "staged", "st_nsplit"):
+        assert i1[key] == i2[key], key
+    Ad, Bd = synth.dyadic_twin(A2, 64, 3)
+    dv = torch_cuda.from_numpy(Ad.vals).cuda()
+    pk = escs.escs_pack(p2, dv)
+    C = torch_cuda.empty(A2.m, 64, device="cuda")
+    escs.escs_spmm_packed(p2, pk, torch_cuda.from_numpy(Bd).cuda(), C)
+    torch_cuda.cuda.synchronize()
+    check_exact(Ad, Bd, C.cpu().numpy())

@@ -77,7 +77,7 @@ def check_schedule(A, n, h, **kw):
             seen = r0 + nr
     assert seen == st["n_rec"] == len(src)
     assert st["n_stage"] == st["n_cta"] * st["max_stages"]
-    assert info["packed_words"] == st["n_rec"] * rw
+    assert info["packed_words"] == (st["n_rec"] * rw + 3) // 4 * 4
     smem = (st["max_k"] * n + st["max_rec"] * rw + st["max_stages"] * st["hdr"].shape[1]) * 4
     assert smem <= 227 * 1024
     return info
