@@ -1068,6 +1068,56 @@ struct TuneKey {
 std::mutex g_tune_mu;
 std::map<TuneKey, std::pair<escs_params, bool>> g_tune_cache;   // params, pdl
 
+// ESCS_TUNE_CACHE_FILE=path: the cache persists across processes (tune once,
+// e.g. before a profiling run that must replay the same plans).  One line per
+// entry: the key's m k nnz bCols device and escs_params words, then the
+// chosen escs_params words and the PDL flag.
+constexpr int kParamWords = (int)(sizeof(escs_params) / sizeof(int32_t));
+const char* tune_cache_file() {
+    const char* f = std::getenv("ESCS_TUNE_CACHE_FILE");
+    return (f && f[0]) ? f : nullptr;
+}
+void tune_cache_load_locked() {
+    static bool loaded = false;
+    if (loaded) return;
+    loaded = true;
+    const char* path = tune_cache_file();
+    if (!path) return;
+    FILE* f = std::fopen(path, "r");
+    if (!f) return;
+    for (;;) {
+        long long m, k, nnz;
+        int bc, dev, pdl;
+        int32_t kq[kParamWords], vq[kParamWords];
+        if (std::fscanf(f, "%lld %lld %lld %d %d", &m, &k, &nnz, &bc, &dev) != 5) break;
+        bool ok = true;
+        for (int i = 0; i < kParamWords && ok; i++) ok = std::fscanf(f, "%d", &kq[i]) == 1;
+        for (int i = 0; i < kParamWords && ok; i++) ok = std::fscanf(f, "%d", &vq[i]) == 1;
+        if (!ok || std::fscanf(f, "%d", &pdl) != 1) break;
+        TuneKey key{m, k, nnz, bc, dev, {}};
+        escs_params v{};
+        std::memcpy(&key.q, kq, sizeof(escs_params));
+        std::memcpy(&v, vq, sizeof(escs_params));
+        g_tune_cache[key] = {v, pdl != 0};
+    }
+    std::fclose(f);
+}
+void tune_cache_append_locked(const TuneKey& key, const escs_params& v, bool pdl) {
+    const char* path = tune_cache_file();
+    if (!path) return;
+    FILE* f = std::fopen(path, "a");
+    if (!f) return;
+    int32_t kq[kParamWords], vq[kParamWords];
+    std::memcpy(kq, &key.q, sizeof(escs_params));
+    std::memcpy(vq, &v, sizeof(escs_params));
+    std::fprintf(f, "%lld %lld %lld %d %d", (long long)key.m, (long long)key.k, (long long)key.nnz, key.bcols,
+                 key.device);
+    for (int i = 0; i < kParamWords; i++) std::fprintf(f, " %d", kq[i]);
+    for (int i = 0; i < kParamWords; i++) std::fprintf(f, " %d", vq[i]);
+    std::fprintf(f, " %d\n", pdl ? 1 : 0);
+    std::fclose(f);
+}
+
 escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                       const int32_t* colidx, int32_t bCols, const escs_params* ep) {
     const char* env = std::getenv("ESCS_AUTOTUNE");
@@ -1088,6 +1138,7 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
         bool found = false;
         {
             std::lock_guard<std::mutex> lk(g_tune_mu);
+            tune_cache_load_locked();
             auto it = g_tune_cache.find(key);
             if (it != g_tune_cache.end()) {
                 hit = it->second;
@@ -1128,7 +1179,9 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
             c.staged = 1;
         }
         std::lock_guard<std::mutex> lk(g_tune_mu);
+        tune_cache_load_locked();
         g_tune_cache[key] = {c, P->dev.pdl};
+        tune_cache_append_locked(key, c, P->dev.pdl);
     }
     return P;
 }

@@ -194,3 +194,21 @@ def test_tuning_cache_reuses_parameters(torch_cuda, monkeypatch):
     escs.escs_spmm_packed(p2, pk, torch_cuda.from_numpy(Bd).cuda(), C)
     torch_cuda.cuda.synchronize()
     check_exact(Ad, Bd, C.cpu().numpy())
+
+
+def test_tuning_cache_file_across_processes(torch_cuda, tmp_path):
+    """ESCS_TUNE_CACHE_FILE: a second process plans with the first one's tuned
+    parameters (autotuned = 2) -- the same plans under a profiler."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2506_15174_b200 import escs, synth\n"
+            "A = synth.magnitude_pruned(256, 512, 0.8, 9)\n"
+            "pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, autotune=1)\n"
+            "i = pl.info; print(i['autotuned'], i['h'], i['T'], i['cta_warps'], i['ufk'], i['colf'])\n") % root
+    env = dict(os.environ, ESCS_TUNE_CACHE_FILE=str(tmp_path / "tune.txt"))
+    out = [subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+           .stdout.split() for _ in range(2)]
+    assert out[0][0] == "1" and out[1][0] == "2"
+    assert out[0][1:] == out[1][1:]

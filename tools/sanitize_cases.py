@@ -2,6 +2,7 @@
 synccheck / initcheck): UFi 1 and 4, vector and scalar lane maps, split and
 heavy panels, empty panels, ragged last panel, long UFi > 1 items (operand
 pipeline), the packed record walk at every UFi with split and heavy panels,
+the staged walk (bulk copies, mbarriers, both combines),
 a grouped launch, the scatter epilogue.  Exits
 non-zero on a mismatch.
 
@@ -74,6 +75,24 @@ def main():
                                 oracle.spmm(A.m, A.k, A.rowptr, A.colidx, Ad.vals, B))
             print("records", n, ufi, prm, "ok" if ok else "MISMATCH", flush=True)
             bad += not ok
+    # the staged walk (TMA bulk copies + mbarriers, in-kernel column-range
+    # combine with the cooperative launch, and the two-launch fallback)
+    S = synth.magnitude_pruned(300, 1100, 0.7, 5)
+    for n, prm in ((128, dict(ufi=8, st_warps=8, st_nsplit=9)), (64, dict(ufi=4, st_warps=6, st_npw=2, st_nsplit=5)),
+                   (32, dict(ufi=1, st_warps=4, st_npw=4, st_nsplit=3)), (128, dict(ufi=3, st_warps=16, st_nsplit=1)),
+                   (128, dict(ufi=2, st_warps=2, st_npw=1, st_nsplit=4))):
+        Ad, B = synth.dyadic_twin(S, n, 13)
+        pl = escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, n, packed=1, staged=2, **prm)
+        pk = escs.escs_pack(pl, torch.from_numpy(Ad.vals).cuda())
+        C = torch.empty(S.m, n, device="cuda")
+        for _ in range(2):   # twice: the combine counters must reset
+            escs.escs_spmm_packed(pl, pk, torch.from_numpy(B).cuda(), C)
+        torch.cuda.synchronize()
+        ok = np.array_equal(C.cpu().numpy().astype(np.float64),
+                            oracle.spmm(S.m, S.k, S.rowptr, S.colidx, Ad.vals, B))
+        print("staged", n, prm, pl.info["st_ctas"], "launches", pl.info["st_launches"], "ok" if ok else "MISMATCH",
+              flush=True)
+        bad += not ok
     # grouped launch: mixed tile widths (idle warps), heavy panels, a UFi-4 single
     probs = [(A0, 64, dict(ufi=1, T=7, cta_warps=3)), (P, 64, dict(ufi=1, T=16, cta_warps=2)),
              (A0, 64, dict(ufi=1, T=9, cta_warps=5)), (W, 64, dict(ufi=4, T=300, cta_warps=4)),

@@ -17,7 +17,7 @@ def main(src, dst, workload="suite", case=None):
             data.append(dict(zip(hdr, r)))
     per = {}
     for d in data:
-        if "esc_spmm_kernel" not in d["Kernel Name"] and "esc_rec_kernel" not in d["Kernel Name"]:
+        if not any(x in d["Kernel Name"] for x in ("esc_spmm_kernel", "esc_rec_kernel", "esc_staged_kernel")):
             continue
         per.setdefault(d["ID"], {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     launches = len(per)
