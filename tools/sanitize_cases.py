@@ -77,10 +77,11 @@ def main():
             bad += not ok
     # the staged walk (TMA bulk copies + mbarriers, in-kernel column-range
     # combine with the cooperative launch, and the two-launch fallback)
-    S = synth.magnitude_pruned(300, 1100, 0.7, 5)
-    for n, prm in ((128, dict(ufi=8, st_warps=8, st_nsplit=9)), (64, dict(ufi=4, st_warps=6, st_npw=2, st_nsplit=5)),
-                   (32, dict(ufi=1, st_warps=4, st_npw=4, st_nsplit=3)), (128, dict(ufi=3, st_warps=16, st_nsplit=1)),
-                   (128, dict(ufi=2, st_warps=2, st_npw=1, st_nsplit=4))):
+    S0 = synth.magnitude_pruned(300, 1100, 0.7, 5)
+    S1 = synth.magnitude_pruned(200, 150, 0.7, 6)   # one column range: no combine
+    for S, n, prm in ((S0, 128, dict(ufi=8, st_warps=8, st_nsplit=9)), (S0, 64, dict(ufi=4, st_warps=6, st_npw=2, st_nsplit=5)),
+                      (S0, 32, dict(ufi=1, st_warps=4, st_npw=4, st_nsplit=3)), (S1, 128, dict(ufi=3, st_warps=16, st_nsplit=1)),
+                      (S0, 128, dict(ufi=2, st_warps=2, st_npw=1, st_nsplit=4))):
         Ad, B = synth.dyadic_twin(S, n, 13)
         pl = escs.escs_plan_ex(S.m, S.k, S.nnz, S.rowptr, S.colidx, n, packed=1, staged=2, **prm)
         pk = escs.escs_pack(pl, torch.from_numpy(Ad.vals).cuda())
