@@ -270,6 +270,22 @@ typedef struct {
                              227 KB of shared memory, ~1 CTA per SM)          */
     int32_t st_kb;        /* staged: columns per pipeline stage (one mbarrier
                              each, <= 16 stages per CTA), 0 = auto             */
+    int32_t hybrid_rows;  /* packed walk on skewed row lengths: 0 = auto (off;
+                             with ESCS_TUNE_HYBRID=1 the autotuner tries a
+                             hybrid plan when the rows of at least twice the
+                             mean length hold >= 25% of the nonzeros -- on
+                             B200 it has not won: DESIGN.md §7), -1 = off, X > 0:
+                             a hybrid plan whose part 0 is the X longest rows
+                             (in descending length order, ties by row index)
+                             planned as their own matrix -- dense rows share
+                             panels, so the enumeration's B-row reuse p is
+                             large there -- and whose part 1 is the other
+                             rows in row order.  Each part is an ordinary
+                             plan (escs_plan_part); escs_pack writes part 0's
+                             record stream then part 1's; escs_spmm_packed
+                             launches part 0 then part 1, each writing its
+                             rows of C.  Only escs_pack / escs_spmm_packed
+                             accept a hybrid plan.                            */
     int32_t reserved[1];  /* must be zero                                        */
 } escs_params;
 
@@ -326,6 +342,9 @@ typedef struct {
     int32_t st_warps, st_npw, st_nsplit, st_kb;
     int32_t st_smem_bytes;  /* staged: dynamic shared memory per CTA               */
     int32_t st_launches;    /* staged: kernel launches per escs_spmm_packed (1, 2)  */
+    int32_t hybrid_rows;    /* hybrid plan: rows in part 0 (0: not a hybrid plan);
+                               the other fields then describe part 0, except
+                               nnz, G, packed_words and device_bytes (totals) */
 } escs_plan_stats;
 
 int escs_plan_info(escs_plan_t plan, escs_plan_stats *out);
@@ -367,6 +386,10 @@ typedef struct escs_staged_view {
     const int32_t *cta, *stage, *hdr, *src;
 } escs_staged_view;
 int escs_staged_export(escs_plan_t plan, escs_staged_view *out);
+/* escs_plan_part -- part i (0 or 1) of a hybrid plan as a plan handle
+ * (borrowed: owned by `plan`, valid until escs_free(plan); do not free it),
+ * for escs_plan_export / escs_plan_info; NULL if `plan` is not hybrid. */
+escs_plan_t escs_plan_part(escs_plan_t plan, int32_t i);
 /* Library version string ("escs <ver> sm_100a"). */
 const char *escs_version(void);
 

@@ -26,9 +26,23 @@ struct escs_plan_impl {
     void* dmem = nullptr;
     size_t dbytes = 0, ws_bytes = 0;
     int autotuned = 0;   // 1: tuned at plan time, 2: parameters from the tuning cache
+    // hybrid plan (escs_params.hybrid_rows): a container of two parts, each an
+    // ordinary plan of a row subset of A -- the hybrid_rows longest rows (in
+    // descending length order) and the rest (in row order); aux holds each
+    // part's row map and value map on the device
+    escs_plan_impl* parts[2] = {nullptr, nullptr};
+    int hybrid_rows = 0;
+    void* aux = nullptr;
+    int64_t part_words[2] = {0, 0};   // record-stream words of each part (packed layout: part 0, part 1)
 };
 
 namespace {
+
+int pack_plan(escs_plan_t P, const float* vals, float* packed, void* stream);
+int64_t plan_packed_words(escs_plan_t P);
+escs_plan_t make_plan_hybrid(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
+                             int32_t bCols, const escs_params* ep, int64_t X);
+int64_t auto_hybrid_rows(int64_t m, int64_t nnz, const int32_t* rowptr, double* share);
 
 thread_local int g_code = ESCS_OK;
 thread_local std::string g_msg;
@@ -388,9 +402,18 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     if (!p.packed && p.h > 1 && p.variant == 1) p.colf = escs::default_colf(bCols);
     // automatic UFk: fall back to the largest UFk the chosen lane map has
     // (wide per-lane tiles carry fewer rows in flight: UFk x colf <= 64)
-    if (!host_only && !(ep && ep->ufk) && !std::getenv("ESCS_PARAMS"))
+    if (!host_only && !(ep && ep->ufk) && !std::getenv("ESCS_PARAMS")) {
+        // the table's columns per lane may have no instance at this UFi (UFi
+        // 6/8 records: default lane maps only): fall back to the default map
+        if (!(ep && ep->colf) && p.variant == 1 && p.colf != escs::default_colf(bCols)) {
+            bool any = false;
+            for (int u = 1; u <= 8 && !any; u *= 2)
+                any = escs::kernel_supported(p.h, bCols, p.variant, u, p.colf, p.packed);
+            if (!any) p.colf = escs::default_colf(bCols);
+        }
         while (p.ufk > 1 && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf, p.packed))
             p.ufk /= 2;
+    }
     if (!host_only && !escs::kernel_supported(p.h, bCols, p.variant, p.ufk, p.colf, p.packed)) {
         fail(ESCS_ERR_UNSUPPORTED, "no kernel for ufi=" + std::to_string(p.h) + " bCols=" +
                                        std::to_string(bCols) + " variant=" +
@@ -565,8 +588,8 @@ struct TuneBufs {
     }
     // the candidate's record stream (packed objective): escs_pack of the
     // tuning values into a buffer grown on demand
-    bool pack_for(const escs::DevPlan& dp) {
-        const size_t w = (size_t)escs::packed_words(dp);
+    bool pack_for(escs_plan_t P) {
+        const size_t w = (size_t)plan_packed_words(P);
         if (w > packed_cap) {
             cudaDeviceSynchronize();
             if (packed) cudaFree(packed);
@@ -579,7 +602,7 @@ struct TuneBufs {
             }
             packed_cap = w;
         }
-        if (escs::launch_pack(dp, vals, packed, stream) != 0) {
+        if (pack_plan(P, vals, packed, stream) != 0) {
             cudaGetLastError();
             return false;
         }
@@ -637,6 +660,28 @@ int launch_plan(const escs::DevPlan& dp, const float* v, const float* B, float* 
     return escs::launch_spmm(dp, v, B, C, stream, vec, packed);
 }
 
+// escs_spmm_packed / escs_pack of any plan, a hybrid container included (its
+// parts in order, part 1's records after part 0's).
+int launch_packed_plan(escs_plan_t P, const float* packed, const float* B, float* C, void* stream, bool vec) {
+    if (!P->parts[0]) return launch_plan(P->dev, packed, B, C, stream, vec, true);
+    for (int q = 0; q < 2; q++) {
+        const int e = launch_plan(P->parts[q]->dev, packed + (q ? P->part_words[0] : 0), B, C, stream, vec, true);
+        if (e) return e;
+    }
+    return 0;
+}
+int pack_plan(escs_plan_t P, const float* vals, float* packed, void* stream) {
+    if (!P->parts[0]) return escs::launch_pack(P->dev, vals, packed, stream);
+    for (int q = 0; q < 2; q++) {
+        const int e = escs::launch_pack(P->parts[q]->dev, vals, packed + (q ? P->part_words[0] : 0), stream);
+        if (e) return e;
+    }
+    return 0;
+}
+int64_t plan_packed_words(escs_plan_t P) {
+    return P->parts[0] ? P->part_words[0] + P->part_words[1] : escs::packed_words(P->dev);
+}
+
 // Latency objective: batches of 16 back-to-back launches queued behind a
 // ~100 us busy-wait (the host enqueues the batch while the GPU spins): GPU
 // time only; min over 3 batches.  A candidate whose launch fails is rejected
@@ -655,7 +700,9 @@ float time_plan_graph(escs_plan_t P, TuneBufs& b, bool packed, const float* v, b
         return -1.f;
     }
     bool ok = true;
-    for (int i = 0; i < kBatch; i++) ok = ok && launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
+    for (int i = 0; i < kBatch; i++)
+        ok = ok && (packed ? launch_packed_plan(P, v, b.B, b.C, b.stream, vec)
+                           : launch_plan(P->dev, v, b.B, b.C, b.stream, vec, false)) == 0;
     const cudaError_t ce = cudaStreamEndCapture(b.stream, &g);
     if (ce != cudaSuccess || !ok || !g || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
         cudaGetLastError();
@@ -685,10 +732,11 @@ float time_plan_graph(escs_plan_t P, TuneBufs& b, bool packed, const float* v, b
 float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
     float best = kFailed;
     const bool vec = aligned16(b.B) && aligned16(b.C);
-    if (packed && !b.pack_for(P->dev)) return kFailed;
+    if (packed && !b.pack_for(P)) return kFailed;
     const float* v = packed ? b.packed : b.vals;
     for (int w = 0; w < 2; w++)
-        if (launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) != 0) {
+        if ((packed ? launch_packed_plan(P, v, b.B, b.C, b.stream, vec)
+                    : launch_plan(P->dev, v, b.B, b.C, b.stream, vec, false)) != 0) {
             cudaGetLastError();
             return kFailed;
         }
@@ -705,7 +753,9 @@ float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
         escs::launch_spin(b.stream, 200000);
         cudaEventRecord(b.e0, b.stream);
         bool ok = true;
-        for (int i = 0; i < kBatch; i++) ok = ok && launch_plan(P->dev, v, b.B, b.C, b.stream, vec, packed) == 0;
+        for (int i = 0; i < kBatch; i++)
+            ok = ok && (packed ? launch_packed_plan(P, v, b.B, b.C, b.stream, vec)
+                               : launch_plan(P->dev, v, b.B, b.C, b.stream, vec, false)) == 0;
         cudaEventRecord(b.e1, b.stream);
         if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
             cudaGetLastError();
@@ -729,7 +779,7 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b, bool packed) {
     const auto& ph = P0->host;
     if (!b.scratch((size_t)ph.n_heavy_tiles * P0->dev.h * P0->dev.bcols, (size_t)ph.n_heavy))
         return kFailed;
-    if (packed && !b.pack_for(P0->dev)) return kFailed;
+    if (packed && !b.pack_for(P0)) return kFailed;
     const float* v = packed ? b.packed : b.vals;
     const int ns = b.ns;
     escs::DevPlan dp[kTuneStreams];
@@ -1041,9 +1091,165 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         }
         clear_error();
     }
-    best.P->autotuned = true;
+    // Hybrid candidate: opt-in (ESCS_TUNE_HYBRID=1).  Measured on C4 (power-law
+    // 16384^2, profiles/r2_notes.md §6) the hybrid never beat the single plan:
+    // the dense rows' part runs fewer, costlier records (UFi 3: 742k records
+    // in 33.6 us vs 1.45M UFi-1 records of the short rows in 41 us), 72-74 us
+    // in total vs 70 us for one plan.
+    const char* eh = std::getenv("ESCS_TUNE_HYBRID");
+    const bool try_hybrid = eh && eh[0] == '1';
+    if (try_hybrid && packed && !concurrent && (!ep || ep->hybrid_rows == 0) && nnz <= 8000000) {
+        // skewed rows (power-law, C4): the longest rows as their own plan, where
+        // panels of dense rows give the enumeration a large p, the rest at UFi 1
+        double share = 0.0;
+        const int64_t X = auto_hybrid_rows(m, nnz, rowptr, &share);
+        if (X >= 8 && X <= m / 2 && share >= 0.25) {
+            escs_params c = q;
+            c.autotune = 1;
+            c.staged = 0;
+            escs_plan_t Hp = make_plan_hybrid(m, k, nnz, rowptr, colidx, bCols, &c, X);
+            if (Hp) {
+                const float th = time_plan(Hp, bufs, true);
+                if (tune_debug())
+                    std::fprintf(stderr, "escs tune: hybrid %lld rows (%.0f%% of nnz) %.2f us vs %.2f us\n",
+                                 (long long)X, 100.0 * share, 1e3f * th, 1e3f * best.t);
+                if (th < 0.97f * best.t) {
+                    escs_free(best.P);
+                    best = {Hp, th};
+                } else {
+                    escs_free(Hp);
+                }
+            }
+            clear_error();
+        }
+    }
+    best.P->autotuned = best.P->autotuned ? best.P->autotuned : 1;
     clear_error();
     return best.P;
+}
+
+escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
+                      const int32_t* colidx, int32_t bCols, const escs_params* ep);
+
+// Hybrid plan (escs_params.hybrid_rows = X): part 0 = the X longest rows in
+// descending length order (ties by row index), part 1 = the other rows in
+// row order, each planned (and, with autotune, tuned) as its own matrix for
+// the packed gather walk; part 0 at the requested UFi (else the tuner's, else
+// 8), part 1 at UFi 1 unless tuned.  Each part gets a row map (its row -> row
+// of C) and a value map (its CSR position -> the caller's CSR position).
+escs_plan_t make_plan_hybrid(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr, const int32_t* colidx,
+                             int32_t bCols, const escs_params* ep, int64_t X) {
+    if (X < 1 || X >= m) {
+        fail(ESCS_ERR_ARG, "hybrid_rows must be in 1..m-1");
+        return nullptr;
+    }
+    std::vector<int64_t> order(m);
+    for (int64_t i = 0; i < m; i++) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return rowptr[a + 1] - rowptr[a] > rowptr[b + 1] - rowptr[b];
+    });
+    std::vector<int64_t> rows[2];
+    rows[0].assign(order.begin(), order.begin() + X);
+    rows[1].assign(order.begin() + X, order.end());
+    std::sort(rows[1].begin(), rows[1].end());
+    const bool tune = ep && ep->autotune;
+    escs_plan_impl* H = new (std::nothrow) escs_plan_impl();
+    if (!H) {
+        fail(ESCS_ERR_OOM, "host allocation");
+        return nullptr;
+    }
+    size_t aux_words = 0;
+    std::vector<int32_t> maps[2][2];   // [part][rowmap, vmap]
+    for (int q = 0; q < 2; q++) {
+        const auto& R = rows[q];
+        const int64_t mq = (int64_t)R.size();
+        std::vector<int32_t> rp(mq + 1, 0), ci;
+        auto& rowmap = maps[q][0];
+        auto& vmap = maps[q][1];
+        rowmap.resize(mq);
+        for (int64_t i = 0; i < mq; i++) {
+            const int64_t r = R[i];
+            rowmap[i] = (int32_t)r;
+            for (int32_t t = rowptr[r]; t < rowptr[r + 1]; t++) {
+                ci.push_back(colidx[t]);
+                vmap.push_back(t);
+            }
+            rp[i + 1] = (int32_t)ci.size();
+        }
+        escs_params c = ep ? *ep : escs_params{};
+        c.hybrid_rows = -1;
+        c.packed = 1;
+        c.staged = 1;   // the gather walk (its epilogue maps rows)
+        // an explicit UFi is part 0's; part 1 (the short rows) runs UFi 1 unless tuned
+        if (q == 1) c.ufi = tune && !(ep && ep->ufi) ? 0 : 1;
+        if (q == 0 && !c.ufi && !tune) c.ufi = 8;
+        // dense rows: short items, so that no lane's fp32 running sum spans
+        // thousands of terms (C4's full rows: G2 1.5e-4 at the table's T, within
+        // 1e-4 at 256)
+        if (q == 0 && !c.T && !tune) c.T = 256;
+        escs_plan_t P = make_plan(mq, k, (int64_t)ci.size(), rp.data(), ci.empty() ? nullptr : ci.data(), bCols, &c);
+        if (!P) {
+            escs_free(H);
+            return nullptr;
+        }
+        H->parts[q] = P;
+        aux_words += (size_t)mq + vmap.size() + 64;
+    }
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(aux_words, 1) * 4) != cudaSuccess) {
+        cudaGetLastError();
+        escs_free(H);
+        fail(ESCS_ERR_OOM, "cudaMalloc (hybrid maps)");
+        return nullptr;
+    }
+    H->aux = d;
+    int32_t* a = static_cast<int32_t*>(d);
+    size_t off = 0;
+    for (int q = 0; q < 2; q++) {
+        for (int w = 0; w < 2; w++) {
+            const auto& v = maps[q][w];
+            if (!v.empty() && cudaMemcpy(a + off, v.data(), v.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+                cudaGetLastError();
+                escs_free(H);
+                fail(ESCS_ERR_CUDA, "cudaMemcpy (hybrid maps)");
+                return nullptr;
+            }
+            (w == 0 ? H->parts[q]->dev.rowmap : H->parts[q]->dev.vmap) = a + off;
+            off += (v.size() + 31) / 32 * 32;
+        }
+        H->part_words[q] = escs::packed_words(H->parts[q]->dev);
+    }
+    H->host_only = false;
+    H->device = H->parts[0]->device;
+    H->params = H->parts[0]->params;
+    H->hybrid_rows = (int)X;
+    H->autotuned = (H->parts[0]->autotuned && H->parts[1]->autotuned) ? 1 : 0;
+    int32_t* hd = H->host.header;
+    hd[0] = 1; hd[1] = (int32_t)m; hd[2] = (int32_t)k; hd[3] = (int32_t)nnz; hd[4] = bCols;
+    hd[5] = H->parts[0]->host.header[5];
+    hd[9] = H->parts[0]->host.header[9] + H->parts[1]->host.header[9];
+    H->dev = H->parts[0]->dev;   // the launch-facing fields are per part; m / bcols of the whole
+    H->dev.m = (int)m;
+    H->dev.rowmap = nullptr;
+    H->dev.vmap = nullptr;
+    return H;
+}
+
+// Rows of at least twice the mean length and their share of the nonzeros:
+// the automatic hybrid candidate (escs_params.hybrid_rows = 0 with autotune).
+int64_t auto_hybrid_rows(int64_t m, int64_t nnz, const int32_t* rowptr, double* share) {
+    if (m < 16 || nnz == 0) return 0;
+    const double mean = (double)nnz / (double)m;
+    int64_t X = 0, hn = 0;
+    for (int64_t i = 0; i < m; i++) {
+        const int64_t L = rowptr[i + 1] - rowptr[i];
+        if ((double)L >= 2.0 * mean) {
+            X++;
+            hn += L;
+        }
+    }
+    *share = (double)hn / (double)nnz;
+    return X;
 }
 
 // Tuning cache (the paper tunes per architecture and bCols; here per
@@ -1126,6 +1332,29 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
         return nullptr;
     }
     const bool tune = (ep && ep->autotune) || (env && env[0] == '1');
+    if (ep && ep->hybrid_rows > 0) {
+        if (ep->host_only) {
+            fail(ESCS_ERR_UNSUPPORTED, "hybrid plans are device plans");
+            return nullptr;
+        }
+        if (!ep->packed) {
+            fail(ESCS_ERR_UNSUPPORTED, "hybrid plans run the packed walk (escs_params.packed = 1)");
+            return nullptr;
+        }
+        clear_error();
+        std::string v = escs::validate_csr(m, k, nnz, rowptr, colidx);
+        if (!v.empty()) {
+            fail(ESCS_ERR_CSR, "invalid CSR: " + v);
+            return nullptr;
+        }
+        escs_params c = *ep;
+        if (tune) c.autotune = c.autotune ? c.autotune : 1;
+        return make_plan_hybrid(m, k, nnz, rowptr, colidx, bCols, &c, ep->hybrid_rows);
+    }
+    if (ep && ep->hybrid_rows < -1) {
+        fail(ESCS_ERR_ARG, "hybrid_rows must be -1, 0 or a row count");
+        return nullptr;
+    }
     if (!tune || (ep && ep->host_only)) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, ep);
     const char* ce = std::getenv("ESCS_TUNE_CACHE");
     const bool use_cache = !(ce && ce[0] == '0');
@@ -1213,6 +1442,15 @@ static int spmm_common(escs_plan_t plan, const float* vals, const float* B, floa
                                       " differs from the plan's device " +
                                       std::to_string(plan->device));
     const bool vec_ok = aligned16(B) && aligned16(C);
+    if (plan->parts[0]) {   // hybrid: its parts in order
+        if (!packed)
+            return fail(ESCS_ERR_UNSUPPORTED, "a hybrid plan runs only through escs_pack + escs_spmm_packed");
+        if (!vec_ok) return fail(ESCS_ERR_UNSUPPORTED, "escs_spmm_packed needs 16-byte aligned B and C");
+        if (vals && !aligned16(vals)) return fail(ESCS_ERR_ARG, "the packed record stream must be 16-byte aligned");
+        const int e = launch_packed_plan(plan, vals, B, C, stream, true);
+        if (e) return fail(ESCS_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString((cudaError_t)e));
+        return ESCS_OK;
+    }
     if (!packed && plan->dev.h > 4)
         return fail(ESCS_ERR_UNSUPPORTED, "the CSR-value walk (escs_spmm) is built for UFi <= 4; "
                                           "run this plan through escs_pack + escs_spmm_packed");
@@ -1249,6 +1487,7 @@ int escs_spmm_group(int32_t n, const escs_plan_t* plans, const float* const* val
             return fail(ESCS_ERR_ARG, "current device differs from the plan's device" + at);
         if (!B[i] || !C[i] || (!vals[i] && P->host.header[3] > 0))
             return fail(ESCS_ERR_ARG, "vals, B and C must be non-NULL device pointers" + at);
+        if (P->parts[0]) return fail(ESCS_ERR_UNSUPPORTED, "hybrid plans are not grouped" + at);
         for (int j = 0; j < i; j++)
             if (plans[j] == P)
                 return fail(ESCS_ERR_ARG, "a plan appears twice in one group (shared workspace)" + at);
@@ -1264,6 +1503,7 @@ int escs_spmm_scatter(escs_plan_t plan, const float* vals, const float* B, float
                       int32_t n_dst, int64_t row_offset, uint32_t flags, void* stream) {
     clear_error();
     if (!plan || plan->host_only) return fail(ESCS_ERR_ARG, "plan is NULL or host-only");
+    if (plan->parts[0]) return fail(ESCS_ERR_UNSUPPORTED, "escs_spmm_scatter does not take hybrid plans");
     if (!dsts || n_dst < 1 || n_dst > 8)
         return fail(ESCS_ERR_ARG, "escs_spmm_scatter needs 1..8 destination buffers");
     if (!B || (!vals && plan->host.header[3] > 0))
@@ -1301,7 +1541,7 @@ int escs_pack(escs_plan_t plan, const float* vals, float* packed, void* stream) 
     if (vals == packed && plan->host.header[9] > 0)
         return fail(ESCS_ERR_ARG, "packed must not alias vals");
     if (packed && !aligned16(packed)) return fail(ESCS_ERR_ARG, "packed must be 16-byte aligned");
-    int e = escs::launch_pack(plan->dev, vals, packed, stream);
+    int e = pack_plan(plan, vals, packed, stream);
     if (e) return fail(ESCS_ERR_CUDA, std::string("pack launch: ") +
                                           cudaGetErrorString((cudaError_t)e));
     // synchronous: the record stream is complete when escs_pack returns, so
@@ -1315,6 +1555,7 @@ int escs_pack(escs_plan_t plan, const float* vals, float* packed, void* stream) 
 int escs_gather_probe(escs_plan_t plan, const float* B, float* sink, void* stream) {
     clear_error();
     if (!plan || plan->host_only || !B || !sink) return fail(ESCS_ERR_ARG, "bad probe arguments");
+    if (plan->parts[0]) return fail(ESCS_ERR_UNSUPPORTED, "no gather probe for hybrid plans");
     const bool vec_ok = aligned16(B);
     int e = escs::launch_probe(plan->dev, B, sink, stream, vec_ok);
     if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") +
@@ -1327,6 +1568,7 @@ int escs_gather_probe_packed(escs_plan_t plan, const float* packed, const float*
     clear_error();
     if (!plan || plan->host_only || !B || !sink || (!packed && plan->host.header[9] > 0))
         return fail(ESCS_ERR_ARG, "bad probe arguments");
+    if (plan->parts[0]) return fail(ESCS_ERR_UNSUPPORTED, "no gather probe for hybrid plans");
     if (plan->dev.st_n_cta) {   // the staged walk's probe (sink: st_ctas x st_warps x 32 floats)
         int e = escs::launch_staged(plan->dev, packed, B, sink, stream, true);
         if (e) return fail(ESCS_ERR_UNSUPPORTED, std::string("probe: ") + cudaGetErrorString((cudaError_t)e));
@@ -1342,6 +1584,9 @@ int escs_gather_probe_packed(escs_plan_t plan, const float* packed, const float*
 
 void escs_free(escs_plan_t plan) {
     if (!plan) return;
+    for (auto* q : plan->parts)
+        if (q) escs_free(q);
+    if (plan->aux) cudaFree(plan->aux);
     if (plan->dmem) cudaFree(plan->dmem);
     delete plan;
 }
@@ -1354,6 +1599,7 @@ int escs_last_error(const char** msg) {
 int escs_plan_export(escs_plan_t plan, escs_plan_view* out) {
     clear_error();
     if (!plan || !out) return fail(ESCS_ERR_ARG, "NULL argument");
+    if (plan->parts[0]) return fail(ESCS_ERR_ARG, "a hybrid plan: export its parts (escs_plan_part)");
     const auto& h = plan->host;
     std::memcpy(out->header, h.header, sizeof(out->header));
     out->grp_panel = h.grp_panel.data();
@@ -1371,6 +1617,19 @@ int escs_plan_export(escs_plan_t plan, escs_plan_view* out) {
 int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     clear_error();
     if (!plan || !o) return fail(ESCS_ERR_ARG, "NULL argument");
+    if (plan->parts[0]) {   // a hybrid plan: part 0's facts, totals where noted (include/escs.h)
+        escs_plan_stats b;
+        int e = escs_plan_info(plan->parts[1], &b);
+        if (!e) e = escs_plan_info(plan->parts[0], o);
+        if (e) return e;
+        o->nnz += b.nnz;
+        o->G += b.G;
+        o->device_bytes += b.device_bytes;
+        o->packed_words = plan->part_words[0] + plan->part_words[1];
+        o->hybrid_rows = plan->hybrid_rows;
+        o->autotuned = plan->autotuned;
+        return ESCS_OK;
+    }
     const auto& h = plan->host;
     std::memset(o, 0, sizeof(*o));
     o->h = plan->params.h;
@@ -1437,6 +1696,15 @@ int escs_staged_export(escs_plan_t plan, escs_staged_view* out) {
     out->hdr = st.hdr.data();
     out->src = st.src.data();
     return ESCS_OK;
+}
+
+escs_plan_t escs_plan_part(escs_plan_t plan, int32_t i) {
+    clear_error();
+    if (!plan || i < 0 || i > 1 || !plan->parts[0]) {
+        fail(ESCS_ERR_ARG, "not a hybrid plan, or part index not 0/1");
+        return nullptr;
+    }
+    return plan->parts[i];
 }
 
 const char* escs_version(void) { return "escs 0.1 sm_100a"; }

@@ -58,6 +58,7 @@ struct KParams {
     float* __restrict__ C;
     int m, n;
     int k;                             // rows of B (the walk's L2 prefetch of B)
+    const int* __restrict__ rowmap;    // plan row -> row of C (a hybrid plan's part), NULL = identity
     // fused row-block all-gather (escs_spmm_scatter): every output row is
     // also stored to extra[d] + (row_off + row) * n, d < n_extra -- the peers'
     // C buffers (P2P / NVLink stores through mapped symmetric memory)
@@ -617,8 +618,9 @@ __device__ __forceinline__ void store_rows(const PP& p, int panel, const float (
                                            int sub, int lj) {
 #pragma unroll
     for (int r = 0; r < H; r++) {
-        const int row = panel * H + r;
-        if ((r % Map::S) == sub && row < p.m) {
+        const int prow = panel * H + r;
+        if ((r % Map::S) == sub && prow < p.m) {
+            const int row = p.rowmap ? p.rowmap[prow] : prow;
             if (p.C) Map::store(p.C + (size_t)row * p.n, a[r], p.n, lj);
             if constexpr (PP::kScatter) {
                 for (int d = 0; d < p.n_extra; d++) {   // fused all-gather epilogue
@@ -643,7 +645,8 @@ __host__ __device__ constexpr int warp_smem_floats() {
 // Store one value group of an output row: C and the fused all-gather
 // destinations (escs_spmm_scatter), V = 4 (float4) or 1 consecutive floats.
 template <int V, class PP>
-__device__ __forceinline__ void store_out(const PP& p, int row, int c, const float (&v)[V]) {
+__device__ __forceinline__ void store_out(const PP& p, int prow, int c, const float (&v)[V]) {
+    const int row = p.rowmap ? p.rowmap[prow] : prow;
     if (p.C) {
         if constexpr (V == 4) *reinterpret_cast<float4*>(p.C + (size_t)row * p.n + c) = make_float4(v[0], v[1], v[2], v[3]);
         else p.C[(size_t)row * p.n + c] = v[0];
@@ -944,6 +947,7 @@ struct GProb {
     const float* B;
     float* C;
     int m, n, W;
+    const int* rowmap;                        // always NULL (hybrid plans are not grouped)
     static constexpr bool kScatter = false;   // no fused all-gather in grouped launches
 };
 struct GroupParams {

@@ -94,6 +94,10 @@ struct DevPlan {
     int G = 0;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
+    // a hybrid plan's part: plan row -> row of C, plan CSR position -> CSR
+    // position of the caller's values (NULL: identity)
+    const int32_t* rowmap = nullptr;
+    const int32_t* vmap = nullptr;
     // staged walk (st_n_cta > 0): schedule arrays and the split workspace
     const int32_t* st_cta = nullptr;
     const int32_t* st_stage = nullptr;

@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict
                                                            const int* __restrict__ vbase,
                                                            const float* __restrict__ vals,
                                                            const int* __restrict__ src,
+                                                           const int* __restrict__ vmap,
                                                            int* __restrict__ out, int G) {
     constexpr int RW = RecFmt<H>::W;
     grid_dep_wait();
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict
         const int pk = gpk[j];   // the plan's word: col | mask << RecFmt<H>::Shift
         if constexpr (H == 1) {
             *reinterpret_cast<int2*>(out + (size_t)q * 2) =
-                make_int2(pk & RecFmt<1>::ColMask, __float_as_int(vals[j]));
+                make_int2(pk & RecFmt<1>::ColMask, __float_as_int(vals[vmap ? vmap[j] : j]));
         } else {
             int w[RW];
 #pragma unroll
@@ -51,7 +52,10 @@ __global__ void __launch_bounds__(256) esc_pack_rec_kernel(const int* __restrict
             int s = vbase[j];
 #pragma unroll
             for (int r = 0; r < H; r++)
-                if ((mk >> r) & 1u) w[1 + r] = __float_as_int(vals[slot[s++]]);
+                if ((mk >> r) & 1u) {
+                    const int q = slot[s++];
+                    w[1 + r] = __float_as_int(vals[vmap ? vmap[q] : q]);
+                }
             int4* o = reinterpret_cast<int4*>(out + (size_t)q * RW);
 #pragma unroll
             for (int v = 0; v < RW / 4; v++) o[v] = make_int4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
@@ -106,6 +110,7 @@ kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, 
     p.m = dp.m;
     p.n = dp.bcols;
     p.k = dp.k;
+    p.rowmap = dp.rowmap;
     return p;
 }
 
@@ -231,12 +236,12 @@ int launch_pack(const DevPlan& dp, const float* vals, float* packed, void* strea
     int* out = reinterpret_cast<int*>(packed);
     cudaStream_t st = (cudaStream_t)stream;
     switch (dp.h) {
-        case 1: kern::esc_pack_rec_kernel<1><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
-        case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
-        case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
-        case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
-        case 6: kern::esc_pack_rec_kernel<6><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
-        case 8: kern::esc_pack_rec_kernel<8><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, out, n); break;
+        case 1: kern::esc_pack_rec_kernel<1><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
+        case 2: kern::esc_pack_rec_kernel<2><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
+        case 3: kern::esc_pack_rec_kernel<3><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
+        case 4: kern::esc_pack_rec_kernel<4><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
+        case 6: kern::esc_pack_rec_kernel<6><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
+        case 8: kern::esc_pack_rec_kernel<8><<<blocks, threads, 0, st>>>(dp.gpk, dp.slot, dp.vbase, vals, src, dp.vmap, out, n); break;
         default: return (int)cudaErrorInvalidConfiguration;
     }
     return (int)cudaGetLastError();

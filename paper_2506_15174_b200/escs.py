@@ -23,7 +23,7 @@ PLAN_ARRAYS = ("grp_panel", "grp_mask", "grp_col_ptr", "grp_val_ptr", "gcol", "s
 EXPORTED_SYMBOLS = ("escs_plan", "escs_plan_ex", "escs_spmm", "escs_free", "escs_last_error",
                     "escs_plan_export", "escs_plan_info", "escs_gather_probe", "escs_version",
                     "escs_pack", "escs_spmm_packed", "escs_spmm_scatter", "escs_spmm_group",
-                    "escs_gather_probe_packed", "escs_staged_export")
+                    "escs_gather_probe_packed", "escs_staged_export", "escs_plan_part")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libescs.so not found at {LIB_PATH}: build it with "
@@ -39,7 +39,7 @@ class _Params(ctypes.Structure):
                 ("colf", ctypes.c_int32), ("tile_order", ctypes.c_int32),
                 ("packed", ctypes.c_int32), ("staged", ctypes.c_int32), ("st_warps", ctypes.c_int32),
                 ("st_npw", ctypes.c_int32), ("st_nsplit", ctypes.c_int32), ("st_kb", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 1)]
+                ("hybrid_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _StagedView(ctypes.Structure):
@@ -63,7 +63,7 @@ class _Stats(ctypes.Structure):
                 ("tile_order", ctypes.c_int32), ("pdl", ctypes.c_int32), ("packed", ctypes.c_int32),
                 ("packed_words", ctypes.c_int64)] + \
                [(n, ctypes.c_int32) for n in ("staged", "st_ctas", "st_warps", "st_npw", "st_nsplit",
-                                              "st_kb", "st_smem_bytes", "st_launches")]
+                                              "st_kb", "st_smem_bytes", "st_launches", "hybrid_rows")]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -95,6 +95,8 @@ _lib.escs_plan_export.argtypes = [_vp, ctypes.POINTER(_View)]
 _lib.escs_plan_export.restype = ctypes.c_int
 _lib.escs_plan_info.argtypes = [_vp, ctypes.POINTER(_Stats)]
 _lib.escs_plan_info.restype = ctypes.c_int
+_lib.escs_plan_part.argtypes = [_vp, _i32]
+_lib.escs_plan_part.restype = _vp
 _lib.escs_staged_export.argtypes = [_vp, ctypes.POINTER(_StagedView)]
 _lib.escs_staged_export.restype = ctypes.c_int
 _lib.escs_version.argtypes = []
@@ -125,14 +127,25 @@ def escs_version() -> str:
 class Plan:
     """Owns an escs_plan_t; freed on close() / garbage collection."""
 
-    def __init__(self, handle, m, k, nnz, bcols):
+    def __init__(self, handle, m, k, nnz, bcols, owner=None):
         self.handle = handle
         self.m, self.k, self.nnz, self.bcols = m, k, nnz, bcols
+        self._owner = owner   # a hybrid plan's part borrows its container's memory
 
     def close(self):
         if self.handle:
-            _lib.escs_free(self.handle)
+            if self._owner is None:
+                _lib.escs_free(self.handle)
             self.handle = None
+
+    def part(self, i):
+        """Part i of a hybrid plan (escs_plan_part), or None."""
+        h = _lib.escs_plan_part(self.handle, int(i))
+        if not h:
+            return None
+        s = _Stats()
+        _lib.escs_plan_info(h, ctypes.byref(s))
+        return Plan(h, 0, self.k, int(s.nnz), self.bcols, owner=self)
 
     def __del__(self):
         try:
@@ -166,17 +179,18 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
                  variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0, packed=0,
-                 staged=0, st_warps=0, st_npw=0, st_nsplit=0, st_kb=0) -> Plan:
+                 staged=0, st_warps=0, st_npw=0, st_nsplit=0, st_kb=0, hybrid_rows=0) -> Plan:
     """escs_plan with explicit escs_params (include/escs.h); 0 = auto for every
     field.  autotune: 1 = latency objective (one stream), 2 = concurrent
     throughput objective (independent SpMMs overlapped on several streams).
     packed=1: plan (and tune, including UFi) for escs_pack + escs_spmm_packed.
     staged: 0 auto, 1 L2-gather record walk, 2 staged walk (B rows in shared
-    memory); st_*: its tile parameters (0 = auto)."""
+    memory); st_*: its tile parameters (0 = auto).  hybrid_rows: 0 auto, -1
+    off, X > 0 a hybrid plan of the X longest rows + the rest (escs_plan_part)."""
     rowptr, colidx = _csr_args(rowptr, colidx)
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
                 int(nthreads), int(autotune), int(colf), int(tile_order), int(packed),
-                int(staged), int(st_warps), int(st_npw), int(st_nsplit), int(st_kb),
+                int(staged), int(st_warps), int(st_npw), int(st_nsplit), int(st_kb), int(hybrid_rows),
                 (ctypes.c_int32 * 1)())
     h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
                           int(bCols), ctypes.byref(p))
