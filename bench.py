@@ -341,7 +341,12 @@ def gather_ceiling(torch, dev, stream):
     return best
 
 
-def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None):
+# L1 / shared-memory wavefronts of one record load (a broadcast 128-bit load
+# costs 2, a 32/64-bit one 1: ncu, profiles/r2_notes.md §4), by UFi
+REC_WAVEFRONTS = {1: 1, 2: 2, 3: 2, 4: 3, 6: 4, 8: 5}
+
+
+def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None, h=None, colf=None):
     """SURVEY §8(d) ceilings of one SpMM (microseconds): compulsory HBM bytes,
     the FP32 FMA pipe, the L1 data path every gathered B row crosses (4*bCols
     bytes per gcol at 128 B/clk/SM; profiles/r2_notes.md §1), and -- when
@@ -354,6 +359,12 @@ def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None):
            "t_hbm_us": bytes_comp / (hbm_gbs * 1e9) * 1e6,
            "t_fma_us": A.nnz * n / (n_sm * 128 * f) * 1e6,
            "t_l1_us": 4.0 * n * G / (n_sm * 128 * f) * 1e6}
+    if h in REC_WAVEFRONTS and colf:
+        # the same data path with the records' own wavefronts: B rows n/32 per
+        # gcol plus the record loads, shared by the S = 32 / (n / colf)
+        # sub-warps whose records one load instruction serves
+        S = max(1, 32 // max(1, n // colf))
+        out["t_l1rec_us"] = G * (n / 32.0 + REC_WAVEFRONTS[h] / S) / (n_sm * f) * 1e6
     if l2_gather_gbs:
         out["t_l2_us"] = 4.0 * n * G / (l2_gather_gbs * 1e9) * 1e6
     return out
@@ -361,7 +372,8 @@ def roofline_bounds(p, G, n_sm, f_mhz, hbm_gbs, l2_gather_gbs=None):
 
 CASE_COLUMNS = ("case", "ufi", "walk", "t_escs_us", "t_escs_csr_us", "t_cusparse_us", "t_cublas_us",
                 "t_cublas_tf32_us", "gflops", "eff_GBps", "pct_hbm", "t_hbm_us", "t_fma_us",
-                "t_l1_us", "t_l2_us", "t_probe_us", "probe_frac", "attainable_frac", "l2_gather_frac", "binding")
+                "t_l1_us", "t_l1rec_us", "t_l2_us", "t_probe_us", "probe_frac", "attainable_frac", "l2_gather_frac",
+                "binding")
 
 
 def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_csr=True, l2_gbs=None):
@@ -422,13 +434,13 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
         t_tf32 = graph_time(torch, lambda: bl.bl_cublas_sgemm(cub, A.m, n, A.k, Ad.data_ptr(), d["B"].data_ptr(), Cd.data_ptr(), 1, sp), stream)
         del Ad
         inf = d["plan"].info
-        rb = roofline_bounds(p, inf["G"], n_sm, f_mhz, hbm_gbs, l2_gbs)
+        rb = roofline_bounds(p, inf["G"], n_sm, f_mhz, hbm_gbs, l2_gbs, h=inf["h"], colf=inf["colf"])
         t_us = 1e3 * t_escs
         # the ceilings are lower bounds on the time (HBM bytes, FMA issue, L1
         # data path); the probe (same walk, no FMAs) is reported beside them
         # as a measurement, not a bound: it is compiled separately and is not
         # guaranteed faster than the kernel
-        bounds = {"hbm": rb["t_hbm_us"], "fma": rb["t_fma_us"], "l1": rb["t_l1_us"]}
+        bounds = {"hbm": rb["t_hbm_us"], "fma": rb["t_fma_us"], "l1": rb.get("t_l1rec_us") or rb["t_l1_us"]}
         binding = max(bounds, key=bounds.get)
         gbps = rb["bytes_comp"] / (t_us * 1e-6) / 1e9
         rows.append({"case": p.name, "ufi": inf["h"], "walk": "staged" if inf["staged"] else "gather", "t_escs_us": t_us,
@@ -439,6 +451,7 @@ def compare_baselines(torch, problems, dev, stream, n_sm, f_mhz, hbm_gbs, with_c
                      "gflops": p.flops / (t_us * 1e-6) / 1e9, "eff_GBps": gbps,
                      "pct_hbm": 100.0 * gbps / hbm_gbs,
                      "t_hbm_us": rb["t_hbm_us"], "t_fma_us": rb["t_fma_us"], "t_l1_us": rb["t_l1_us"],
+                     "t_l1rec_us": rb.get("t_l1rec_us"),
                      "t_probe_us": 1e3 * t_probe if t_probe else None,
                      "probe_frac": (1e3 * t_probe / t_us) if t_probe else None,
                      "attainable_frac": bounds[binding] / t_us, "binding": binding,
@@ -915,7 +928,8 @@ def run_escs(args):
             l2_gbs = gather_ceiling(torch, device, stream)
         except (OSError, AssertionError):
             l2_gbs = None
-        rb = roofline_bounds(pd, dd["G"], n_sm, f_mhz, hbm, l2_gbs)
+        rb = roofline_bounds(pd, dd["G"], n_sm, f_mhz, hbm, l2_gbs, h=dd["plan"].info["h"],
+                             colf=dd["plan"].info["colf"])
         t_dom_us = 1e3 * float(per_prob[dom])
         dom_gbs = rb["bytes_comp"] / (t_dom_us * 1e-6) / 1e9
         clocks = clk.summary()
@@ -972,6 +986,11 @@ def run_escs(args):
                                       "what": "4*bCols bytes per gcol (plan G) through 128 B/clk/SM at the max SM clock "
                                               "(profiles/r2_notes.md 1): the ceiling that binds, not HBM"},
                 "t_fma_us": rb["t_fma_us"], "t_hbm_us": rb["t_hbm_us"],
+                "l1_wavefront_ceiling": None if "t_l1rec_us" not in rb else {
+                    "t_us": rb["t_l1rec_us"], "frac": rb["t_l1rec_us"] / t_dom_us,
+                    "what": "L1 / shared-memory wavefronts of the B rows (bCols/32 per gcol) and of the record loads "
+                            "(1-5 per record by UFi, per sub-warp group) at one wavefront per clk per SM: the data "
+                            "path both walks are bound by"},
                 "l2_gather_ceiling": None if l2_gbs is None else {
                     "measured_GBps": l2_gbs, "t_l2_us": rb["t_l2_us"], "frac": rb["t_l2_us"] / t_dom_us,
                     "what": "4*bCols bytes per gcol at the measured L2->SM random 512-byte-row gather rate "
