@@ -1037,6 +1037,11 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         const bool fixed_h = ep && ep->ufi;
         for (int h : {1, 2, 3, 4, 6, 8}) {
             if (fixed_h ? h != ep->ufi : (h > 4 && dens < 0.15)) continue;   // UFi 6/8 where p is large
+            // the expected B-row reuse of UFi h on a uniformly pruned matrix,
+            // p = h d / (1 - (1 - d)^h): below 1.1 a UFi > 1 plan only adds
+            // record bytes and predicated FMA slots (never chosen in the B200
+            // suite sweeps) -- not searched
+            if (!fixed_h && h > 1 && h * dens / (1.0 - std::pow(1.0 - dens, h)) < 1.1) continue;
             const double sp = (double)k * (1.0 - std::pow(1.0 - dens, h));
             const int pw[6][2] = {{1, 0}, {3, 0}, {8, 4}, {8, 16}, {24, 4}, {24, 16}};
             for (const auto& x : pw) {
@@ -1057,7 +1062,10 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
                 per_h[h] = {};
             }
         Cand r1 = per_h[1].P ? refine(per_h[1]) : Cand{};
-        Cand rb = (hb != 1 && per_h[hb].P) ? refine(per_h[hb]) : Cand{};
+        // the best UFi > 1 is refined only if it is within 10% of the refined
+        // UFi-1 plan already (refinement gains are a few percent)
+        Cand rb = (hb != 1 && per_h[hb].P && (!r1.P || per_h[hb].t < 1.10f * r1.t)) ? refine(per_h[hb]) : Cand{};
+        if (hb != 1 && per_h[hb].P && !rb.P) escs_free(per_h[hb].P);
         if (rb.P && (!r1.P || rb.t < 0.97f * r1.t)) {
             if (r1.P) escs_free(r1.P);
             best = rb;
