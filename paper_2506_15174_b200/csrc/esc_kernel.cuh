@@ -557,6 +557,9 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* q, uint32_t bytes) 
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(q), "r"(bytes) : "memory");
 }
 
+#ifndef ESC_REC_BPF
+#define ESC_REC_BPF 1
+#endif
 #ifndef ESC_REC_L2PF
 #define ESC_REC_L2PF 0   // measured: no gain on the cold step, +0.2-0.4 us on the small hot layers
 #endif
@@ -590,8 +593,24 @@ __device__ __forceinline__ void walk_rec(const PP& p, int beg, int end, float (&
         prefetch_l2_bulk(a0, (uint32_t)(((b1 - a0) + 15) & ~15));
     }
 #endif
+#if ESC_REC_BPF
+    // This CTA's share of B into L2, BEFORE the programmatic-dependent-launch
+    // wait: an L2 prefetch is only a hint and L2 is the device's point of
+    // coherence, so a line the previous kernel is still writing is never seen
+    // stale (L1 is not filled); the DRAM fetch of a cold B then overlaps the
+    // previous kernel's tail instead of the walk's first gathers.
+    if (lane == 0 && (threadIdx.x >> 5) == 0 && p.k > 0) {
+        const size_t total = (size_t)p.k * p.n * 4;
+        const size_t chunk = ((total + gridDim.x - 1) / gridDim.x + 255) & ~size_t(255);
+        const size_t off = (size_t)blockIdx.x * chunk;
+        if (off < total) {
+            const size_t len = (total - off < chunk ? total - off : chunk);
+            prefetch_l2_bulk(reinterpret_cast<const char*>(p.B) + off, (uint32_t)((len + 15) & ~size_t(15)));
+        }
+    }
+#endif
     grid_dep_wait();
-#if ESC_REC_L2PF
+#if ESC_REC_L2PF && !ESC_REC_BPF
     // this CTA's share of B into L2 (B is caller data: after the wait); every
     // row is gathered by many warps, most of them on other SMs
     if (lane == 0 && (threadIdx.x >> 5) == 0 && p.k > 0) {

@@ -1,7 +1,7 @@
 // Instantiations of the staged record walk (staged_kernel.cuh) for lane map
 // VecMap<16, 8> (bCols 128): UFi 1, 2, 3, 4, 6, 8 (the record formats of
 // esc_kernel.cuh RecFmt), panels per warp NPW with NPW x UFi x F <= 32
-// accumulators per lane, UFk = 4 records per sub-warp in flight; each with
+// accumulators per lane (UFi 6 / 8: 48 / 64), UFk = 4 records per sub-warp in flight; each with
 // its gather probe (same loads, no FMAs).
 #include "staged_kernel.cuh"
 
@@ -19,9 +19,11 @@ StagedFn get_staged_b128_f8(int h, int npw, bool probe) {
     ESC_ST_CASE(2, 1) ESC_ST_CASE(2, 2) ESC_ST_CASE(2, 4)
     ESC_ST_CASE(3, 1) ESC_ST_CASE(3, 2)
     ESC_ST_CASE(4, 1) ESC_ST_CASE(4, 2)
-    ESC_ST_CASE(6, 1)
-    ESC_ST_CASE(8, 1)
 #undef ESC_ST_CASE
+    // UFi 6 / 8 on the two-sub-warp map: 48 / 64 accumulators per lane (128
+    // registers, no spills); one record load instruction serves two records
+    if (h == 6 && npw == 1) return probe ? esc_staged_kernel<6, M, U, 1, true> : esc_staged_kernel<6, M, U, 1, false>;
+    if (h == 8 && npw == 1) return probe ? esc_staged_kernel<8, M, U, 1, true> : esc_staged_kernel<8, M, U, 1, false>;
     return nullptr;
 }
 

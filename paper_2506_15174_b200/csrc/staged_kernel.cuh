@@ -305,6 +305,9 @@ __global__ void ESC_ST_BOUNDS esc_staged_kernel(const __grid_constant__ SParams 
             // before the programmatic-dependent-launch wait
             if (hbytes) bulk_g2s(sH, p.hdr + (size_t)sbase * p.hs, hbytes, &bar[0], pol_first);
             if (rbytes) bulk_g2s(sR + (size_t)(st.z - rec0) * RW, p.rec + (size_t)st.z * RW, rbytes, &bar[lane], pol_first);
+            // B's stage rows into L2 already (a hint; L2 is coherent, L1 is not
+            // filled), so the copies below, after the wait, hit L2 on a cold B
+            if (bbytes) prefetch_l2_bulk(p.B + (size_t)st.x * N, bbytes);
         }
         grid_dep_wait();   // B is caller data written by the previous kernel
         if (lane < nst && bbytes)
