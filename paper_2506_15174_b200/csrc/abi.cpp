@@ -160,7 +160,7 @@ constexpr size_t kStSmemCap = 227 * 1024 - 8 * 1024 - 512;   // static: mbarrier
 
 // Auto tile of the staged walk: 16 warps x 1 panel per CTA (fewer when the
 // matrix has fewer panels), column ranges so that about one CTA per SM runs
-// (the B range plus the records fill most of the 227 KB), stages of ~16 KB of
+// (the B range plus the records fill most of the 227 KB), stages of ~32 KB of
 // B rows (at most 16).  build_staged then checks the budget; the caller
 // raises nsplit while it does not fit.
 void auto_staged(escs::Params& p, const escs::PlanHost& ph, int bcols, int n_sm) {
@@ -186,7 +186,9 @@ void auto_staged(escs::Params& p, const escs::PlanHost& ph, int bcols, int n_sm)
     }
     if (!p.st_kb) {
         const int64_t wd = (k + p.st_nsplit - 1) / p.st_nsplit;
-        const int64_t kb = std::max<int64_t>(8, 16384 / (4 * bcols));
+        // ~32 KB of B rows per stage (dominant layer: 16 KB stages 17.9 us,
+        // 32 KB 17.1 us; profiles/r2_notes.md §4)
+        const int64_t kb = std::max<int64_t>(8, 32768 / (4 * bcols));
         p.st_kb = (int)std::max<int64_t>(kb, (wd + 15) / 16);
     }
 }

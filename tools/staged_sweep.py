@@ -59,15 +59,18 @@ def main():
         best = None
         if a.configs:
             for cfg in a.configs.split(";"):
-                h, W, npw, ns = (int(x) for x in cfg.split(","))
+                v = [int(x) for x in cfg.split(",")]
+                h, W, npw, ns = v[:4]
+                colf = v[4] if len(v) > 4 else 0
+                kb = v[5] if len(v) > 5 else 0
                 try:
                     pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, ufi=h, packed=1, staged=2,
-                                           st_warps=W, st_npw=npw, st_nsplit=ns)
+                                           st_warps=W, st_npw=npw, st_nsplit=ns, colf=colf, st_kb=kb)
                 except escs.EscsError as ex:
                     print(f"  {name} h{h} W{W} npw{npw} ns{ns}: {ex}", flush=True)
                     continue
                 t, err = run(pl)
-                print(f"  {name} h{h} W{W} npw{npw} ns{ns} ctas {pl.info['st_ctas']} L{pl.info['st_launches']} "
+                print(f"  {name} h{h} W{W} npw{npw} ns{pl.info['st_nsplit']} kb{pl.info['st_kb']} F{pl.info['colf']} ctas {pl.info['st_ctas']} L{pl.info['st_launches']} "
                       f"{t*1e3:7.2f} us err {err:.1e}", flush=True)
                 res.append({"case": name, "h": h, "warps": W, "npw": npw, "nsplit": ns, "us": t * 1e3, "err": err})
                 pl.close()
