@@ -501,6 +501,10 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
             return nullptr;
         }
         int e = escs::prepare_kernels(dp);
+        {   // L1 for the gathered B rows: the carveout that just holds the walk's occupancy
+            const char* lm = std::getenv("ESCS_L1MAX");
+            if (!e && !(lm && lm[0] == '0')) dp.carveout = escs::gather_carveout(dp, p.packed != 0);
+        }
         if (!e && dp.st_n_cta) {
             e = escs::prepare_staged(dp);
             // the split combine runs in the walk kernel when the whole grid

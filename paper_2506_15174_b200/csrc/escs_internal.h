@@ -94,6 +94,8 @@ struct DevPlan {
     int G = 0;
     bool any_sync = false;
     bool pdl = true;                    // programmatic dependent launch (ESCS_PDL=0 disables)
+    int carveout = -1;                  // preferred shared-memory carveout (percent) of the gather
+                                        // walk's launches, -1 = the driver's choice
     // a hybrid plan's part: plan row -> row of C, plan CSR position -> CSR
     // position of the caller's values (NULL: identity)
     const int32_t* rowmap = nullptr;
@@ -142,5 +144,7 @@ int launch_spin(void* stream, long long cycles);   // tuner: busy-wait on the st
 size_t smem_bytes(const DevPlan& dp, bool packed = false);
 // Resident CTAs per SM for this plan's launch configuration.
 int blocks_per_sm(const DevPlan& dp, bool vec, bool probe, bool packed = false);
+// The gather walk's preferred carveout for this plan (percent shared memory).
+int gather_carveout(const DevPlan& dp, bool packed);
 
 }  // namespace escs
