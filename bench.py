@@ -609,8 +609,8 @@ def run_escs(args):
                 d["plan"], d["packed"], d["B"], d["C"] if C is None else C, st))(d)
             sink = torch.empty(max(1, info["n_tiles"] * 32 * info["cta_warps"], info["st_ctas"] * 32 * info["st_warps"]),
                                device=device)
-            d["probe"] = (lambda d, sink: lambda st: escs.escs_gather_probe_packed(
-                d["plan"], d["packed"], d["B"], sink, st))(d, sink)
+            d["probe"] = ((lambda d, sink: lambda st: escs.escs_gather_probe_packed(
+                d["plan"], d["packed"], d["B"], sink, st))(d, sink) if not info["hybrid_rows"] else None)
         else:
             d["run"] = (lambda d: lambda st, C=None: escs.escs_spmm(
                 d["plan"], d["vals"], d["B"], d["C"] if C is None else C, st))(d)

@@ -362,7 +362,9 @@ int escs_gather_probe(escs_plan_t plan, const float *B, float *sink, void *strea
  * escs_gather_probe_packed -- the same for escs_spmm_packed: the record walk
  * (one broadcast record load per column, the 128-bit B-row gathers) without
  * the FMAs.  `packed` is the record stream of escs_pack (only the column
- * words are used).  Same sink contract.
+ * words are used).  Same sink contract; for a staged plan the staged walk's
+ * probe (the same bulk copies and shared-memory reads, no FMAs) with `sink`
+ * float[st_ctas * 32 * st_warps].  Hybrid plans: ESCS_ERR_UNSUPPORTED.
  */
 int escs_gather_probe_packed(escs_plan_t plan, const float *packed, const float *B, float *sink,
                              void *stream);

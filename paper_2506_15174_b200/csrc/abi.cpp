@@ -782,6 +782,9 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b, bool packed) {
     const bool vec = aligned16(b.B) && aligned16(b.C);
     // the copies share the read-only plan arrays; each has its own workspace
     // and counters (one plan must not run on two streams at once)
+    // staged and hybrid plans keep per-plan state the copies would share (the
+    // column-range partials and counters; two parts): not timed concurrently
+    if (P0->dev.st_n_cta || P0->parts[0]) return kFailed;
     const auto& ph = P0->host;
     if (!b.scratch((size_t)ph.n_heavy_tiles * P0->dev.h * P0->dev.bcols, (size_t)ph.n_heavy))
         return kFailed;
