@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -650,6 +651,16 @@ struct TuneBufs {
 
 constexpr float kFailed = 1e30f;
 
+double g_tune_build_s = 0.0, g_tune_time_s = 0.0;   // ESCS_TUNE_DEBUG accounting
+long g_tune_cands = 0;
+struct TuneReport {
+    ~TuneReport() {
+        if (g_tune_cands)
+            std::fprintf(stderr, "escs tune: %ld candidates, %.2f s building plans, %.2f s timing\n", g_tune_cands,
+                         g_tune_build_s, g_tune_time_s);
+    }
+} g_tune_report;
+
 bool tune_debug() {
     static const bool on = [] {
         const char* e = std::getenv("ESCS_TUNE_DEBUG");
@@ -924,13 +935,22 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         return concurrent ? time_plans_concurrent(P, bufs, packed) : time_plan(P, bufs, packed);
     };
     auto build = [&](escs_params c) -> Cand {
+        const auto t0 = std::chrono::steady_clock::now();
         escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+        const auto t1 = std::chrono::steady_clock::now();
         if (!P) {
             clear_error();
             return {};
         }
         if (concurrent) P->dev.pdl = false;
-        return {P, timed(P)};
+        const float t = timed(P);
+        if (tune_debug()) {
+            const auto t2 = std::chrono::steady_clock::now();
+            g_tune_build_s += std::chrono::duration<double>(t1 - t0).count();
+            g_tune_time_s += std::chrono::duration<double>(t2 - t1).count();
+            g_tune_cands++;
+        }
+        return {P, t};
     };
     auto keep = [](Cand& cur, Cand x) {   // cur = the faster of cur and x (the other is freed)
         if (!x.P) return;

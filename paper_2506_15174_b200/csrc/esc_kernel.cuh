@@ -107,6 +107,15 @@ __device__ __forceinline__ float ld_stream_f(const float* p) {
     return r;
 }
 
+// L1 eviction priorities of the gathered B rows and of the record loads
+// (experiment hooks; empty = the default, evict_normal)
+#ifndef ESC_B_L1
+#define ESC_B_L1 ""
+#endif
+#ifndef ESC_REC_L1
+#define ESC_REC_L1 ""
+#endif
+
 // Vector lane map: L lanes own one gathered B row of N = L*F floats (F
 // consecutive floats per lane, 128-bit loads for F >= 4), so a warp gathers
 // S = 32/L rows per step ("sub-warps"); sub-warp partial sums are reduced
@@ -152,7 +161,7 @@ struct VecMap {
         } else {
 #pragma unroll
             for (int v = 0; v < F / 4; v++)
-                asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                asm volatile("ld.global.nc" ESC_B_L1 ".L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                              : "=f"(b[4 * v]), "=f"(b[4 * v + 1]), "=f"(b[4 * v + 2]),
                                "=f"(b[4 * v + 3])
                              : "l"(q + 4 * v * L), "l"(pol));
@@ -487,11 +496,11 @@ struct RecFmt {
 template <int RW, int NW>
 __device__ __forceinline__ void ld_rec(int (&r)[RW], const int* q) {
     if constexpr (RW == 2) {
-        asm volatile("ld.global.nc.v2.s32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "l"(q));
+        asm volatile("ld.global.nc" ESC_REC_L1 ".v2.s32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "l"(q));
     } else {
 #pragma unroll
         for (int v = 0; v < NW / 4; v++)
-            asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];"
+            asm volatile("ld.global.nc" ESC_REC_L1 ".v4.s32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(r[4 * v]), "=r"(r[4 * v + 1]), "=r"(r[4 * v + 2]), "=r"(r[4 * v + 3])
                          : "l"(q + 4 * v));
         constexpr int R = NW % 4, B0 = NW - R;
