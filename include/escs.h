@@ -286,6 +286,13 @@ typedef struct {
                              launches part 0 then part 1, each writing its
                              rows of C.  Only escs_pack / escs_spmm_packed
                              accept a hybrid plan.                            */
+    int32_t carveout;     /* the gather walk's preferred shared-memory carveout
+                             per launch: 0 = auto (the smallest that holds the
+                             plan's occupancy -- the rest of the SM's 228 KB is
+                             L1 for re-read B rows; the autotuner also times
+                             smaller carveouts, trading occupancy for L1),
+                             1..100 = that percent, -1 = the driver's choice,
+                             -2 = 0 percent (maximum L1)                      */
     int32_t reserved[1];  /* must be zero                                        */
 } escs_params;
 
@@ -342,6 +349,7 @@ typedef struct {
     int32_t st_warps, st_npw, st_nsplit, st_kb;
     int32_t st_smem_bytes;  /* staged: dynamic shared memory per CTA               */
     int32_t st_launches;    /* staged: kernel launches per escs_spmm_packed (1, 2)  */
+    int32_t carveout;       /* the gather walk's launch carveout in percent (-1: driver) */
     int32_t hybrid_rows;    /* hybrid plan: rows in part 0 (0: not a hybrid plan);
                                the other fields then describe part 0, except
                                nnz, G, packed_words and device_bytes (totals) */

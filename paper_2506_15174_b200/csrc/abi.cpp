@@ -329,6 +329,10 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
             fail(ESCS_ERR_ARG, "escs_params.packed must be 0 or 1");
             return nullptr;
         }
+        if (ep->carveout < -2 || ep->carveout > 100) {
+            fail(ESCS_ERR_ARG, "escs_params.carveout must be -2..100");
+            return nullptr;
+        }
     }
     std::string v = escs::validate_csr(m, k, nnz, rowptr, colidx);
     if (!v.empty()) {
@@ -504,7 +508,10 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         int e = escs::prepare_kernels(dp);
         {   // L1 for the gathered B rows: the carveout that just holds the walk's occupancy
             const char* lm = std::getenv("ESCS_L1MAX");
-            if (!e && !(lm && lm[0] == '0')) dp.carveout = escs::gather_carveout(dp, p.packed != 0);
+            const int cv = ep ? ep->carveout : 0;
+            if (!e && cv == 0 && !(lm && lm[0] == '0')) dp.carveout = escs::gather_carveout(dp, p.packed != 0);
+            else if (cv > 0) dp.carveout = std::min(cv, 100);
+            else if (cv == -2) dp.carveout = 0;
         }
         if (!e && dp.st_n_cta) {
             e = escs::prepare_staged(dp);
@@ -1103,6 +1110,26 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             best = r1;
         }
     }
+    if (!concurrent && !(ep && ep->carveout) && !best.P->dev.st_n_cta && best.P->dev.carveout > 0) {
+        // L1 against occupancy: the same plan with smaller carveouts (fewer
+        // resident CTAs, more L1 for re-read B rows); kept at a 2% margin
+        const int cv0 = best.P->dev.carveout;
+        int cv_best = cv0;
+        float t_best = best.t;
+        for (int cv : {0, cv0 / 2}) {
+            if (cv >= cv0) continue;
+            best.P->dev.carveout = cv;
+            const float t = timed(best.P);
+            if (tune_debug()) std::fprintf(stderr, "escs tune: carveout %d%%: %.2f us (vs %d%%: %.2f us)\n", cv,
+                                           1e3f * t, cv0, 1e3f * best.t);
+            if (t < 0.98f * t_best) {
+                t_best = t;
+                cv_best = cv;
+            }
+        }
+        best.P->dev.carveout = cv_best;
+        best.t = t_best;
+    }
     if (want_st == 0 && best.P->dev.variant == 1 && (bCols == 32 || bCols == 64 || bCols == 128) &&
         (double)nnz >= 0.15 * (double)m * (double)k && (double)nnz * bCols >= 4.0e7) {
         // the staged walk where its B-row reuse in shared memory can pay:
@@ -1435,6 +1462,7 @@ escs_plan_t make_plan(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
         c.colf = P->dev.variant == 1 ? P->params.colf : 0;
         c.tile_order = P->params.tile_order;
         c.packed = P->params.packed;
+        c.carveout = P->dev.carveout < 0 ? -1 : (P->dev.carveout == 0 ? -2 : P->dev.carveout);
         if (P->host.st.n_cta) {
             c.staged = 2;
             c.st_warps = P->host.st.warps;
@@ -1694,6 +1722,7 @@ int escs_plan_info(escs_plan_t plan, escs_plan_stats* o) {
     o->colf = plan->dev.variant == 1 ? plan->params.colf : 0;
     o->tile_order = plan->params.tile_order;
     o->pdl = plan->dev.pdl ? 1 : 0;
+    o->carveout = plan->dev.carveout;
     {
         escs::DevPlan d = plan->dev;   // host-only plans: the same formula from the header
         d.h = h.header[5];

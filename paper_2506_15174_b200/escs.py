@@ -39,7 +39,7 @@ class _Params(ctypes.Structure):
                 ("colf", ctypes.c_int32), ("tile_order", ctypes.c_int32),
                 ("packed", ctypes.c_int32), ("staged", ctypes.c_int32), ("st_warps", ctypes.c_int32),
                 ("st_npw", ctypes.c_int32), ("st_nsplit", ctypes.c_int32), ("st_kb", ctypes.c_int32),
-                ("hybrid_rows", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("hybrid_rows", ctypes.c_int32), ("carveout", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class _StagedView(ctypes.Structure):
@@ -63,7 +63,7 @@ class _Stats(ctypes.Structure):
                 ("tile_order", ctypes.c_int32), ("pdl", ctypes.c_int32), ("packed", ctypes.c_int32),
                 ("packed_words", ctypes.c_int64)] + \
                [(n, ctypes.c_int32) for n in ("staged", "st_ctas", "st_warps", "st_npw", "st_nsplit",
-                                              "st_kb", "st_smem_bytes", "st_launches", "hybrid_rows")]
+                                              "st_kb", "st_smem_bytes", "st_launches", "carveout", "hybrid_rows")]
 
 
 _vp, _i64, _i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
@@ -179,7 +179,7 @@ def escs_plan(m, k, nnz, rowptr, colidx, bCols) -> Plan:
 
 def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, cta_warps=0,
                  variant=0, ufk=0, nthreads=0, autotune=0, colf=0, tile_order=0, packed=0,
-                 staged=0, st_warps=0, st_npw=0, st_nsplit=0, st_kb=0, hybrid_rows=0) -> Plan:
+                 staged=0, st_warps=0, st_npw=0, st_nsplit=0, st_kb=0, hybrid_rows=0, carveout=0) -> Plan:
     """escs_plan with explicit escs_params (include/escs.h); 0 = auto for every
     field.  autotune: 1 = latency objective (one stream), 2 = concurrent
     throughput objective (independent SpMMs overlapped on several streams).
@@ -191,7 +191,7 @@ def escs_plan_ex(m, k, nnz, rowptr, colidx, bCols, *, ufi=0, T=0, host_only=0, c
     p = _Params(int(ufi), int(T), int(host_only), int(cta_warps), int(variant), int(ufk),
                 int(nthreads), int(autotune), int(colf), int(tile_order), int(packed),
                 int(staged), int(st_warps), int(st_npw), int(st_nsplit), int(st_kb), int(hybrid_rows),
-                (ctypes.c_int32 * 1)())
+                int(carveout), (ctypes.c_int32 * 1)())
     h = _lib.escs_plan_ex(int(m), int(k), int(nnz), rowptr.ctypes.data, colidx.ctypes.data,
                           int(bCols), ctypes.byref(p))
     if not h:
