@@ -10,7 +10,11 @@ namespace kern {
 
 StagedFn get_staged_b128_f8(int h, int npw, bool probe) {
     using M = VecMap<16, 8>;
+#ifdef ESC_ST_U
+    constexpr int U = ESC_ST_U;
+#else
     constexpr int U = 4;
+#endif
 #define ESC_ST_CASE(H_, NPW_)                                                             \
     if constexpr ((NPW_) * (H_) * M::F <= 32)                                             \
         if (h == (H_) && npw == (NPW_))                                                   \
