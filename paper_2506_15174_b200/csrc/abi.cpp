@@ -1375,16 +1375,21 @@ void tune_cache_load_locked() {
 void tune_cache_append_locked(const TuneKey& key, const escs_params& v, bool pdl) {
     const char* path = tune_cache_file();
     if (!path) return;
-    FILE* f = std::fopen(path, "a");
-    if (!f) return;
     int32_t kq[kParamWords], vq[kParamWords];
     std::memcpy(kq, &key.q, sizeof(escs_params));
     std::memcpy(vq, &v, sizeof(escs_params));
-    std::fprintf(f, "%lld %lld %lld %d %d", (long long)key.m, (long long)key.k, (long long)key.nnz, key.bcols,
-                 key.device);
-    for (int i = 0; i < kParamWords; i++) std::fprintf(f, " %d", kq[i]);
-    for (int i = 0; i < kParamWords; i++) std::fprintf(f, " %d", vq[i]);
-    std::fprintf(f, " %d\n", pdl ? 1 : 0);
+    // the whole line in one write (O_APPEND-style): processes sharing the file
+    // never interleave inside an entry
+    std::string line = std::to_string((long long)key.m) + " " + std::to_string((long long)key.k) + " " +
+                       std::to_string((long long)key.nnz) + " " + std::to_string(key.bcols) + " " +
+                       std::to_string(key.device);
+    for (int i = 0; i < kParamWords; i++) line += " " + std::to_string(kq[i]);
+    for (int i = 0; i < kParamWords; i++) line += " " + std::to_string(vq[i]);
+    line += pdl ? " 1\n" : " 0\n";
+    FILE* f = std::fopen(path, "a");
+    if (!f) return;
+    std::setvbuf(f, nullptr, _IONBF, 0);
+    std::fwrite(line.data(), 1, line.size(), f);
     std::fclose(f);
 }
 
