@@ -212,3 +212,25 @@ def test_tuning_cache_file_across_processes(torch_cuda, tmp_path):
            .stdout.split() for _ in range(2)]
     assert out[0][0] == "1" and out[1][0] == "2"
     assert out[0][1:] == out[1][1:]
+
+
+@pytest.mark.parametrize("cv", [-2, -1, 25, 100])
+def test_explicit_carveout_exact(torch_cuda, cv):
+    """escs_params.carveout only changes the L1 / shared split of the launches:
+    the result is bitwise the same as the automatic carveout's."""
+    from paper_2506_15174_b200 import escs
+    A = synth.magnitude_pruned(512, 1024, 0.8, 77)
+    Ad, Bd = synth.dyadic_twin(A, 64, 5)
+    outs = []
+    for c in (0, cv):
+        pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, carveout=c, T=40, cta_warps=4)
+        exp_cv = {0: None, -2: 0, -1: -1}.get(c, c)
+        if exp_cv is not None:
+            assert pl.info["carveout"] == exp_cv
+        pk = escs.escs_pack(pl, torch_cuda.from_numpy(Ad.vals).cuda())
+        C = torch_cuda.empty(A.m, 64, device="cuda")
+        escs.escs_spmm_packed(pl, pk, torch_cuda.from_numpy(Bd).cuda(), C)
+        torch_cuda.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    check_exact(Ad, Bd, outs[1])

@@ -146,3 +146,20 @@ def test_schedule_deterministic():
     b = escs.escs_staged_export(staged_plan(p.A, 64, ufi=4, nthreads=8))
     for key in ("cta", "stage", "hdr", "src"):
         assert np.array_equal(a[key], b[key])
+
+
+def test_hybrid_and_carveout_parameter_errors():
+    """Host-side checks of the hybrid_rows and carveout fields (include/escs.h)."""
+    A = synth.power_law(200, 300, 0.9, 3)
+    with pytest.raises(escs.EscsError) as e:   # hybrid plans are device plans
+        escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, host_only=1, hybrid_rows=10)
+    assert e.value.code == escs.ESCS_ERR_UNSUPPORTED
+    with pytest.raises(escs.EscsError) as e:
+        escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, host_only=1, hybrid_rows=-5)
+    assert e.value.code == escs.ESCS_ERR_ARG
+    for cv in (-3, 101):
+        with pytest.raises(escs.EscsError) as e:
+            escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, host_only=1, carveout=cv)
+        assert e.value.code == escs.ESCS_ERR_ARG
+    for cv in (-2, -1, 0, 37, 100):   # accepted (host-only plans launch nothing)
+        escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 64, packed=1, host_only=1, carveout=cv)
