@@ -193,7 +193,9 @@ int escs_spmm_scatter(escs_plan_t plan, const float *vals, const float *B,
 /* escs_free -- release the plan's host and device memory (the plan owns them,
  * "TA" of Listing 2, kept until the caller drops it).  NULL is a
  * no-op.  No call on the plan may be in flight (the caller synchronises the
- * streams that used it, as with cudaFree). */
+ * streams that used it, as with cudaFree).  Autotuned plans take their device
+ * memory from a private stream-ordered pool (up to 1 GiB of freed memory is
+ * kept for later plans); escs_free then waits for the device, like cudaFree. */
 void escs_free(escs_plan_t plan);
 
 /* Code and message of the last failed call on this thread (ESCS_OK and ""

@@ -27,6 +27,7 @@ struct escs_plan_impl {
     void* dmem = nullptr;
     size_t dbytes = 0, ws_bytes = 0;
     int autotuned = 0;   // 1: tuned at plan time, 2: parameters from the tuning cache
+    bool pooled = false; // device memory from the planner's stream-ordered pool (autotuned plans)
     // hybrid plan (escs_params.hybrid_rows): a container of two parts, each an
     // ordinary plan of a row subset of A -- the hybrid_rows longest rows (in
     // descending length order) and the rest (in row order); aux holds each
@@ -194,6 +195,53 @@ void auto_staged(escs::Params& p, const escs::PlanHost& ph, int bcols, int n_sm)
     }
 }
 
+double g_tune_build_s = 0.0, g_tune_time_s = 0.0;   // ESCS_TUNE_DEBUG accounting
+double g_dbg_upload_s = 0.0, g_dbg_prepare_s = 0.0, g_dbg_host_s = 0.0, g_dbg_free_s = 0.0;
+long g_tune_cands = 0;
+struct TuneReport {
+    ~TuneReport() {
+        if (g_tune_cands)
+            std::fprintf(stderr, "escs tune: %ld candidates, %.2f s building plans (host %.2f, upload %.2f, "
+                                 "kernel attributes %.2f), %.2f s timing, %.2f s freeing\n", g_tune_cands,
+                         g_tune_build_s, g_dbg_host_s, g_dbg_upload_s, g_dbg_prepare_s, g_tune_time_s, g_dbg_free_s);
+    }
+} g_tune_report;
+
+bool tune_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("ESCS_TUNE_DEBUG");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// The autotuner builds and frees thousands of candidate plans: cudaMalloc /
+// cudaFree per candidate (the latter synchronising the device) was ~10 s of the
+// suite's ~24 s of planning (ESCS_TUNE_DEBUG accounting).  Autotuned plans
+// therefore take their memory from a private stream-ordered pool (retained up
+// to 1 GiB), allocated and freed on the legacy stream.
+cudaMemPool_t plan_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(device);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        pool = nullptr;
+    } else {
+        uint64_t keep = 1ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pools[device] = pool;
+    return pool;
+}
+
 bool upload(escs_plan_impl* P) {
     auto& ph = P->host;
     auto& dp = P->dev;
@@ -255,7 +303,17 @@ bool upload(escs_plan_impl* P) {
     const size_t o_stk = add_region<int32_t>(off, 2 * st_rb);
     off = std::max<size_t>(off, 256);
     void* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, off);
+    cudaError_t e = cudaErrorMemoryAllocation;
+    if (P->pooled) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaMemPool_t pool = plan_pool(dev)) {
+            e = cudaMallocFromPoolAsync(&d, off, pool, 0);
+            if (e != cudaSuccess) cudaGetLastError();
+        }
+        if (e != cudaSuccess) P->pooled = false;
+    }
+    if (!P->pooled) e = cudaMalloc(&d, off);
     if (e != cudaSuccess) {
         fail(e == cudaErrorMemoryAllocation ? ESCS_ERR_OOM : ESCS_ERR_CUDA,
              std::string("cudaMalloc(") + std::to_string(off) + "): " + cudaGetErrorString(e));
@@ -305,7 +363,8 @@ bool upload(escs_plan_impl* P) {
 }
 
 escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
-                            const int32_t* colidx, int32_t bCols, const escs_params* ep) {
+                            const int32_t* colidx, int32_t bCols, const escs_params* ep,
+                            bool pooled = false) {
     clear_error();
     if (m < 1 || k < 1 || nnz < 0 || bCols < 1) {
         fail(ESCS_ERR_ARG, "m, k, bCols must be >= 1 and nnz >= 0");
@@ -483,6 +542,7 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     P->params = p;
     P->host_only = host_only;
     P->device = device;
+    P->pooled = pooled && !host_only;
     auto& dp = P->dev;
     dp.m = (int)m; dp.k = (int)k; dp.nnz = (int)nnz; dp.bcols = bCols; dp.h = p.h;
     dp.n_tiles = P->host.n_tiles; dp.cta_warps = p.cta_warps; dp.variant = p.variant;
@@ -501,10 +561,12 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         dp.pdl = !(e && e[0] == '0');
     }
     if (!host_only) {
+        const auto tu0 = std::chrono::steady_clock::now();
         if (!upload(P)) {
             escs_free(P);
             return nullptr;
         }
+        const auto tu1 = std::chrono::steady_clock::now();
         int e = escs::prepare_kernels(dp);
         {   // L1 for the gathered B rows: the carveout that just holds the walk's occupancy
             const char* lm = std::getenv("ESCS_L1MAX");
@@ -522,6 +584,12 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
             const int nb = e ? 0 : escs::staged_blocks_per_sm(dp);
             dp.st_coop = !(ec && ec[0] == '0') && nb > 0 &&
                          (int64_t)dp.st_n_cta <= (int64_t)nb * sm_count_of_current_device();
+        }
+        if (tune_debug()) {
+            const auto tu2 = std::chrono::steady_clock::now();
+            g_dbg_upload_s += std::chrono::duration<double>(tu1 - tu0).count();
+            g_dbg_prepare_s += std::chrono::duration<double>(tu2 - tu1).count();
+            g_dbg_host_s += P->host.plan_seconds;
         }
         if (e) {
             fail(ESCS_ERR_CUDA, std::string("kernel attributes: ") +
@@ -658,23 +726,7 @@ struct TuneBufs {
 
 constexpr float kFailed = 1e30f;
 
-double g_tune_build_s = 0.0, g_tune_time_s = 0.0;   // ESCS_TUNE_DEBUG accounting
-long g_tune_cands = 0;
-struct TuneReport {
-    ~TuneReport() {
-        if (g_tune_cands)
-            std::fprintf(stderr, "escs tune: %ld candidates, %.2f s building plans, %.2f s timing\n", g_tune_cands,
-                         g_tune_build_s, g_tune_time_s);
-    }
-} g_tune_report;
 
-bool tune_debug() {
-    static const bool on = [] {
-        const char* e = std::getenv("ESCS_TUNE_DEBUG");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
 
 // One SpMM launch of whichever walk the plan runs (the staged walk for a
 // staged plan's record stream).
@@ -731,6 +783,8 @@ float time_plan_graph(escs_plan_t P, TuneBufs& b, bool packed, const float* v, b
     if (ce != cudaSuccess || !ok || !g || cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) {
         cudaGetLastError();
         if (g) cudaGraphDestroy(g);
+        cudaStreamSynchronize(b.stream);
+        cudaGetLastError();
         return -1.f;
     }
     float best = kFailed;
@@ -740,6 +794,8 @@ float time_plan_graph(escs_plan_t P, TuneBufs& b, bool packed, const float* v, b
         ok = cudaGraphLaunch(ge, b.stream) == cudaSuccess;
         cudaEventRecord(b.e1, b.stream);
         if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            cudaStreamSynchronize(b.stream);
             cudaGetLastError();
             best = kFailed;
             break;
@@ -762,6 +818,8 @@ float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
         if ((packed ? launch_packed_plan(P, v, b.B, b.C, b.stream, vec)
                     : launch_plan(P->dev, v, b.B, b.C, b.stream, vec, false)) != 0) {
             cudaGetLastError();
+            cudaStreamSynchronize(b.stream);   // nothing of the candidate left in flight
+            cudaGetLastError();
             return kFailed;
         }
     static const bool graph = [] {
@@ -782,6 +840,8 @@ float time_plan(escs_plan_t P, TuneBufs& b, bool packed) {
                                : launch_plan(P->dev, v, b.B, b.C, b.stream, vec, false)) == 0;
         cudaEventRecord(b.e1, b.stream);
         if (cudaEventSynchronize(b.e1) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            cudaStreamSynchronize(b.stream);
             cudaGetLastError();
             return kFailed;
         }
@@ -860,6 +920,18 @@ float time_plans_concurrent(escs_plan_t P0, TuneBufs& b, bool packed) {
 // from the B200 sweeps (profiles/r2_notes.md "staged walk"), column ranges
 // automatic (about one co-resident CTA per SM); explicit parameters are not
 // searched.  Returns the fastest, or NULL.
+// Free a tuner candidate: its launches were synchronised by the timing, so
+// its pooled memory goes back to the pool without a device-wide wait.
+void free_candidate(escs_plan_t P) {
+    if (P && P->pooled && !P->parts[0] && !P->aux) {
+        if (P->dmem) cudaFreeAsync(P->dmem, 0);
+        P->dmem = nullptr;
+        delete P;
+        return;
+    }
+    escs_free(P);
+}
+
 escs_plan_t make_plan_staged_tuned(int64_t m, int64_t k, int64_t nnz, const int32_t* rowptr,
                                    const int32_t* colidx, int32_t bCols, escs_params q, TuneBufs* shared) {
     q.autotune = 0;
@@ -869,7 +941,7 @@ escs_plan_t make_plan_staged_tuned(int64_t m, int64_t k, int64_t nnz, const int3
     TuneBufs* bufs = shared;
     if (!bufs) {
         own.reset(new TuneBufs(m, k, nnz, bCols, false));
-        if (!own->ok) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+        if (!own->ok) return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q, true);
         bufs = own.get();
     }
     static const int cand[][3] = {{8, 16, 1}, {4, 16, 2}, {6, 8, 1}, {4, 8, 1}, {3, 16, 1}, {2, 16, 1}};
@@ -885,7 +957,7 @@ escs_plan_t make_plan_staged_tuned(int64_t m, int64_t k, int64_t nnz, const int3
             dup = dup || ((q.ufi ? q.ufi : (*y)[0]) == c.ufi && (q.st_warps ? q.st_warps : (*y)[1]) == c.st_warps &&
                           (q.st_npw ? q.st_npw : (*y)[2]) == c.st_npw);
         if (dup) continue;
-        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c, true);
         if (!P) {
             if (tune_debug()) std::fprintf(stderr, "escs tune: staged h%d W%d npw%d: %s\n", c.ufi, c.st_warps, c.st_npw, g_msg.c_str());
             clear_error();
@@ -896,18 +968,18 @@ escs_plan_t make_plan_staged_tuned(int64_t m, int64_t k, int64_t nnz, const int3
             std::fprintf(stderr, "escs tune: staged h%d W%d npw%d ns%d ctas %d coop %d: %.2f us\n", c.ufi, c.st_warps,
                          c.st_npw, P->host.st.nsplit, P->host.st.n_cta, (int)P->dev.st_coop, 1e3f * t);
         if (t < bt) {
-            if (best) escs_free(best);
+            if (best) free_candidate(best);
             best = P;
             bt = t;
         } else {
-            escs_free(P);
+            free_candidate(P);
         }
     }
     if (best) {
         best->autotuned = true;
         clear_error();
     } else if (!shared) {
-        return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);   // reports why
+        return make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q, true);   // reports why
     }
     return best;
 }
@@ -924,7 +996,7 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     const int want_st = (packed && !concurrent) ? q.staged : 1;
     if (want_st == 2) return make_plan_staged_tuned(m, k, nnz, rowptr, colidx, bCols, q, nullptr);
     q.staged = 1;
-    escs_plan_t first = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q);
+    escs_plan_t first = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q, true);
     // Throughput plans launch without programmatic dependent launch: with
     // many streams sharing the SMs, CTAs that start early and wait on the
     // previous grid hold SM slots the other streams' layers could use (suite
@@ -943,7 +1015,7 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     };
     auto build = [&](escs_params c) -> Cand {
         const auto t0 = std::chrono::steady_clock::now();
-        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c);
+        escs_plan_t P = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &c, true);
         const auto t1 = std::chrono::steady_clock::now();
         if (!P) {
             clear_error();
@@ -961,12 +1033,14 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     };
     auto keep = [](Cand& cur, Cand x) {   // cur = the faster of cur and x (the other is freed)
         if (!x.P) return;
+        const auto f0 = std::chrono::steady_clock::now();
         if (x.t < cur.t) {
-            if (cur.P) escs_free(cur.P);
+            if (cur.P) free_candidate(cur.P);
             cur = x;
         } else {
-            escs_free(x.P);
+            free_candidate(x.P);
         }
+        if (tune_debug()) g_dbg_free_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - f0).count();
     };
     // the parameters of a plan as an escs_params candidate base
     auto params_of = [&](escs_plan_t P) {
@@ -1094,19 +1168,19 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             if (per_h[h].P && (!hb || per_h[h].t < per_h[hb].t)) hb = h;
         for (int h = 1; h <= 8; h++)   // keep only the best UFi and UFi = 1
             if (per_h[h].P && h != hb && h != 1) {
-                escs_free(per_h[h].P);
+                free_candidate(per_h[h].P);
                 per_h[h] = {};
             }
         Cand r1 = per_h[1].P ? refine(per_h[1]) : Cand{};
         // the best UFi > 1 is refined only if it is within 10% of the refined
         // UFi-1 plan already (refinement gains are a few percent)
         Cand rb = (hb != 1 && per_h[hb].P && (!r1.P || per_h[hb].t < 1.10f * r1.t)) ? refine(per_h[hb]) : Cand{};
-        if (hb != 1 && per_h[hb].P && !rb.P) escs_free(per_h[hb].P);
+        if (hb != 1 && per_h[hb].P && !rb.P) free_candidate(per_h[hb].P);
         if (rb.P && (!r1.P || rb.t < 0.97f * r1.t)) {
-            if (r1.P) escs_free(r1.P);
+            if (r1.P) free_candidate(r1.P);
             best = rb;
         } else {
-            if (rb.P) escs_free(rb.P);
+            if (rb.P) free_candidate(rb.P);
             best = r1;
         }
     }
@@ -1147,10 +1221,10 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
                 std::fprintf(stderr, "escs tune: best staged %.2f us vs gather walk %.2f us (h%d)\n", 1e3f * ts,
                              1e3f * best.t, best.P->params.h);
             if (ts < 0.97f * best.t) {
-                escs_free(best.P);
+                free_candidate(best.P);
                 best = {S, ts};
             } else {
-                escs_free(S);
+                free_candidate(S);
             }
         }
         clear_error();
@@ -1178,10 +1252,10 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
                     std::fprintf(stderr, "escs tune: hybrid %lld rows (%.0f%% of nnz) %.2f us vs %.2f us\n",
                                  (long long)X, 100.0 * share, 1e3f * th, 1e3f * best.t);
                 if (th < 0.97f * best.t) {
-                    escs_free(best.P);
+                    free_candidate(best.P);
                     best = {Hp, th};
                 } else {
-                    escs_free(Hp);
+                    free_candidate(Hp);
                 }
             }
             clear_error();
@@ -1657,7 +1731,16 @@ void escs_free(escs_plan_t plan) {
     for (auto* q : plan->parts)
         if (q) escs_free(q);
     if (plan->aux) cudaFree(plan->aux);
-    if (plan->dmem) cudaFree(plan->dmem);
+    if (plan->dmem) {
+        if (plan->pooled) {
+            // the caller's streams may be non-blocking: wait for the device as
+            // cudaFree would, then return the memory to the planner's pool
+            cudaDeviceSynchronize();
+            cudaFreeAsync(plan->dmem, 0);
+        } else {
+            cudaFree(plan->dmem);
+        }
+    }
     delete plan;
 }
 
