@@ -1126,23 +1126,11 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         return cur;
     };
 
-    Cand best;
-    if (!packed) {
-        best = refine({first, timed(first)});
-    } else {
-        // Stage 0 (record walk): UFi jointly with the item size and the tile
-        // width -- the paper's tuner searches UFi first; on B200
-        // the best UFi > 1 plans need short items in narrow tiles (many warps
-        // per panel, combined through the workspace), which a descent that
-        // fixes T before W never reaches (profiles/r2_notes.md).  Items per
-        // panel {1, 3, 8, 24} x tile width {auto, 4, 16}, from the expected
-        // panel stream k(1 - s^h) of a uniformly pruned matrix.  Then the
-        // best UFi and UFi = 1 are each refined; a UFi > 1 plan is kept only
-        // if it beats the refined UFi = 1 plan by 3% (its split panels combine
-        // through the workspace, which the hot timing undercounts on a cold
-        // L2: bench steps flush it).
+    // The packed walk's search (stage 0 + refinement), from a start plan.
+    auto packed_search = [&](escs_plan_t start) -> Cand {
+        Cand out;
         Cand per_h[9];
-        per_h[first->params.h] = {first, timed(first)};
+        per_h[start->params.h] = {start, timed(start)};
         const double dens = (double)nnz / ((double)m * (double)k);
         const bool fixed_h = ep && ep->ufi;
         for (int h : {1, 2, 3, 4, 6, 8}) {
@@ -1178,10 +1166,41 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
         if (hb != 1 && per_h[hb].P && !rb.P) free_candidate(per_h[hb].P);
         if (rb.P && (!r1.P || rb.t < 0.97f * r1.t)) {
             if (r1.P) free_candidate(r1.P);
-            best = rb;
+            out = rb;
         } else {
             if (rb.P) free_candidate(rb.P);
-            best = r1;
+            out = r1;
+        }
+        return out;
+    };
+    Cand best;
+    if (!packed) {
+        best = refine({first, timed(first)});
+    } else {
+        best = packed_search(first);
+        // A second search for a nearly all-L1 SM (2% carveout: the smallest
+        // shared-memory configuration, fewer resident CTAs) where B fits in L1
+        // (<= 256 KB): with a fixed carveout the tuned plans differ in T, W
+        // and UFk (2048x512@70% b128: 10.3 -> 9.4 us hot; profiles/r2_notes.md
+        // §10); kept at a 2% margin
+        if (!concurrent && !(ep && ep->carveout) && (int64_t)k * bCols * 4 <= 256 * 1024 &&
+            best.P->dev.variant == 1) {
+            const escs_params q0 = q;
+            q.carveout = 2;
+            escs_plan_t first2 = make_plan_fixed(m, k, nnz, rowptr, colidx, bCols, &q, true);
+            if (first2) {
+                Cand l1 = packed_search(first2);
+                if (tune_debug() && l1.P)
+                    std::fprintf(stderr, "escs tune: L1 search %.2f us vs %.2f us\n", 1e3f * l1.t, 1e3f * best.t);
+                if (l1.P && l1.t < 0.98f * best.t) {
+                    free_candidate(best.P);
+                    best = l1;
+                } else if (l1.P) {
+                    free_candidate(l1.P);
+                }
+            }
+            clear_error();
+            q = q0;
         }
     }
     if (!concurrent && !(ep && ep->carveout) && !best.P->dev.st_n_cta && best.P->dev.carveout > 0) {
