@@ -207,6 +207,17 @@ struct TuneReport {
     }
 } g_tune_report;
 
+// B sizes for which the tuner also searches at a 2% carveout: above 96 KB (a
+// smaller B fits L1 at any carveout: the second search never won) and up to
+// ESCS_L1_FIT_KB (default 320: wins at 128-288 KB, rare beyond; notes §10)
+int64_t l1_fit_bytes() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("ESCS_L1_FIT_KB");
+        return (int64_t)(e ? std::atoi(e) : 320) * 1024;
+    }();
+    return v;
+}
+
 bool tune_debug() {
     static const bool on = [] {
         const char* e = std::getenv("ESCS_TUNE_DEBUG");
@@ -1179,11 +1190,12 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
     } else {
         best = packed_search(first);
         // A second search for a nearly all-L1 SM (2% carveout: the smallest
-        // shared-memory configuration, fewer resident CTAs) where B fits in L1
-        // (<= 256 KB): with a fixed carveout the tuned plans differ in T, W
+        // shared-memory configuration, fewer resident CTAs) where B about fits
+        // in L1 (96-320 KB): with a fixed carveout the tuned plans differ in T, W
         // and UFk (2048x512@70% b128: 10.3 -> 9.4 us hot; profiles/r2_notes.md
         // §10); kept at a 2% margin
-        if (!concurrent && !(ep && ep->carveout) && (int64_t)k * bCols * 4 <= 256 * 1024 &&
+        const int64_t bbytes = (int64_t)k * bCols * 4;
+        if (!concurrent && !(ep && ep->carveout) && bbytes > 96 * 1024 && bbytes <= l1_fit_bytes() &&
             best.P->dev.variant == 1) {
             const escs_params q0 = q;
             q.carveout = 2;
