@@ -246,8 +246,14 @@ typedef struct {
     int32_t tile_order;   /* CTA tile formation: 0 = auto (by item length when the
                              panel work is skewed, p99 >= 2x median), 1 = panel
                              order, 2 = panels ordered by their longest item
-                             (similar work per tile, long tiles first).
-                             Searched by the autotuner when 0.               */
+                             (similar work per tile, long tiles first), 3 =
+                             column windows (UFi 1 only): a tile holds item j
+                             of W consecutive panels, so an SM walks one
+                             column window of many rows; a split panel's items
+                             combine through per-item workspace slots and a
+                             per-panel counter (last arriver sums in item
+                             order).  1 and 2 are searched by the autotuner
+                             when 0.                                         */
     int32_t packed;       /* 1: the plan will run through escs_pack +
                              escs_spmm_packed (the record walk): the parameter
                              table and the autotuner target that walk, and

@@ -304,6 +304,9 @@ bool upload(escs_plan_impl* P) {
     const size_t ws_elems = (size_t)ph.n_heavy_tiles * h * n;
     const size_t o_ws = add_region<float>(off, ws_elems);
     const auto& st = ph.st;
+    const size_t o_sws = add_region<int32_t>(off, ph.slot_ws.size());
+    const size_t o_wscc = add_region<int32_t>(off, ph.n_wsc_counters);
+    const size_t o_wsc = add_region<float>(off, (size_t)ph.wsc_floats);
     const size_t o_stc = add_region<int32_t>(off, st.cta.size());
     const size_t o_sts = add_region<int32_t>(off, st.stage.size());
     const size_t o_sth = add_region<int32_t>(off, st.hdr.size());
@@ -332,7 +335,7 @@ bool upload(escs_plan_impl* P) {
     }
     P->dmem = d;
     P->dbytes = off;
-    P->ws_bytes = (ws_elems + st_ws) * sizeof(float);
+    P->ws_bytes = (ws_elems + st_ws + (size_t)ph.wsc_floats) * sizeof(float);
     char* b = static_cast<char*>(d);
     auto put = [&](size_t o, const void* src, size_t bytes) -> bool {
         if (!bytes) return true;
@@ -347,6 +350,13 @@ bool upload(escs_plan_impl* P) {
     if (!put(o_tiles, ph.tile_heavy.data(), ph.tile_heavy.size() * 4)) return false;
     if (!put(o_heavy, ph.heavy_info.data(), ph.heavy_info.size() * 4)) return false;
     if (ph.n_heavy) CUDA_TRY(cudaMemset(b + o_cnt, 0, ph.n_heavy * 4));
+    if (!ph.slot_ws.empty()) {
+        if (!put(o_sws, ph.slot_ws.data(), ph.slot_ws.size() * 4)) return false;
+        if (ph.n_wsc_counters) CUDA_TRY(cudaMemset(b + o_wscc, 0, (size_t)ph.n_wsc_counters * 4));
+        dp.slot_ws = reinterpret_cast<const int32_t*>(b + o_sws);
+        dp.wsc_counters = reinterpret_cast<int32_t*>(b + o_wscc);
+        dp.wsc = reinterpret_cast<float*>(b + o_wsc);
+    }
     if (!put(o_stc, st.cta.data(), st.cta.size() * 4)) return false;
     if (!put(o_sts, st.stage.data(), st.stage.size() * 4)) return false;
     if (!put(o_sth, st.hdr.data(), st.hdr.size() * 4)) return false;
@@ -443,10 +453,10 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
     // bounds); up to 28 for the record walk (72 registers x 28 x 32 <= 64K)
     const int max_warps = p.packed ? 28 : 16;
     if (p.h < 1 || p.h > 16 || p.T < 1 || (set_warps && (p.cta_warps < 1 || p.cta_warps > max_warps)) ||
-        p.variant < 1 || p.variant > 2 || p.tile_order < 0 || p.tile_order > 2 ||
+        p.variant < 1 || p.variant > 2 || p.tile_order < 0 || p.tile_order > 3 ||
         !(p.colf == 0 || p.colf == 4 || p.colf == 8 || p.colf == 16)) {
         fail(ESCS_ERR_ARG, "parameters out of range (ufi 1..16, T >= 1, cta_warps 1..16 (1..28 packed), "
-                           "variant 1..2, colf 0/4/8/16, tile_order 0..2)");
+                           "variant 1..2, colf 0/4/8/16, tile_order 0..3)");
         return nullptr;
     }
     if (p.variant == 1 && !(bCols == 4 || bCols == 8 || bCols == 16 || bCols == 32 || bCols == 64 ||
@@ -509,8 +519,12 @@ escs_plan_t make_plan_fixed(int64_t m, int64_t k, int64_t nnz, const int32_t* ro
         const char* to = std::getenv("ESCS_TILE_ORDER");   // "panel" | "length" override
         if (to && std::string(to) == "panel") p.tile_order = 1;
         else if (to && std::string(to) == "length") p.tile_order = 2;
-        if (p.tile_order < 1 || p.tile_order > 2) p.tile_order = auto_tile_order(P->host);
-        escs::build_tiles(P->host, p.cta_warps, p.tile_order == 2);
+        if (p.tile_order == 3 && p.h != 1) p.tile_order = 1;   // column windows: UFi 1 (column-ordered streams)
+        if (p.tile_order < 1 || p.tile_order > 3) p.tile_order = auto_tile_order(P->host);
+        if (p.tile_order == 3)
+            escs::build_tiles_cols(P->host, p.cta_warps, bCols);
+        else
+            escs::build_tiles(P->host, p.cta_warps, p.tile_order == 2);
         if (p.staged == 2) {
             // lane map of the staged walk: the plan's columns per lane if that
             // instance exists, else 4
@@ -1133,6 +1147,9 @@ escs_plan_t make_plan_autotuned(int64_t m, int64_t k, int64_t nnz, const int32_t
             escs_params c = params_of(cur.P);
             c.tile_order = cur.P->params.tile_order == 2 ? 1 : 2;
             keep(cur, build(c));
+            // (column windows, tile_order 3, are not searched: chosen by the hot
+            // timing on six 2048x512 layers, they lost on the cold step --
+            // profiles/r2_notes.md §11)
         }
         return cur;
     };

@@ -59,6 +59,9 @@ struct KParams {
     int m, n;
     int k;                             // rows of B (the walk's L2 prefetch of B)
     const int* __restrict__ rowmap;    // plan row -> row of C (a hybrid plan's part), NULL = identity
+    const int4* __restrict__ slot_ws;  // column-window tiles: per slot {ws offset, counter, items, ordinal}
+    float* wsc;                        // column-window tiles: per-item partials
+    int* wsc_counters;
     // fused row-block all-gather (escs_spmm_scatter): every output row is
     // also stored to extra[d] + (row_off + row) * n, d < n_extra -- the peers'
     // C buffers (P2P / NVLink stores through mapped symmetric memory)
@@ -787,6 +790,52 @@ __device__ __forceinline__ void heavy_combine(const PP& p, const float* smem, in
     if (tid == 0) p.counters[th.x] = 0;   // self-reset: graph replay safe
 }
 
+// Column-window tiles (tile_order 3): the warps of a CTA hold item j of W
+// different panels -- one column window of W panels, whose B rows the SM
+// re-reads from L1.  A split panel's items therefore sit in different CTAs:
+// each warp stores its item's partial (h x bCols) in the workspace slot of
+// (panel, item), releases it on the panel's counter, and the last item to
+// arrive sums the panel's partials in item order and writes C (deterministic;
+// per warp, no CTA barrier; the counter resets itself).
+template <int H, class Map, class PP>
+__device__ __forceinline__ void item_ws_combine(const PP& p, float (&acc)[H][Map::F], int slot, int panel,
+                                                int sub, int lj, int lane) {
+    constexpr int F = Map::F, S = Map::S;
+    const int n = p.n;
+    const int4 sw = p.slot_ws[slot];   // ws offset, counter, items of the panel, this item's ordinal
+    float* mine = p.wsc + sw.x;
+#pragma unroll
+    for (int r = 0; r < H; r++)
+        if ((r % S) == sub) Map::store(mine + (size_t)r * n, acc[r], n, lj);
+    __threadfence();
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(p.wsc_counters + sw.y, 1) == sw.z - 1;
+    last = __shfl_sync(kFull, last, 0);
+    if (!last) return;
+    __threadfence();
+    const float* base = p.wsc + sw.x - (size_t)sw.w * H * n;   // the panel's item 0
+#pragma unroll
+    for (int r = 0; r < H; r++) {
+        if ((r % S) != sub) continue;
+        float a[F];
+#pragma unroll
+        for (int f = 0; f < F; f++) a[f] = 0.f;
+        for (int q = 0; q < sw.z; q++) {
+            const float* row = base + (size_t)q * H * n + (size_t)r * n;
+#pragma unroll
+            for (int v = 0; v < F / 4; v++) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(row + 4 * (F <= 4 ? lj : v * Map::L + lj)));
+                a[4 * v] += x.x; a[4 * v + 1] += x.y; a[4 * v + 2] += x.z; a[4 * v + 3] += x.w;
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < F; f++) acc[r][f] = a[f];
+    }
+    store_rows<H, Map, PP>(p, panel, acc, sub, lj);
+    if (lane == 0) p.wsc_counters[sw.y] = 0;   // graph replay safe
+}
+
 // One CTA tile.  Item slots are tile-major: tile t owns slots [t*W, t*W + W),
 // W = warps per CTA; slot aux = lead | cnt << 8 | active << 16 | tile_sync << 17
 // | tile_heavy << 18 (lead: warp of the panel's first item in this tile, cnt:
@@ -829,6 +878,12 @@ __device__ __forceinline__ void process_tile(const PP& p, float* smem, int tile,
 #pragma unroll
                     for (int off = Map::L; off < 32; off <<= 1)
                         acc[r][f] += __shfl_xor_sync(kFull, acc[r][f], off);
+        }
+    }
+    if constexpr (!(MODE == kProbe || MODE == kRecProbe)) {
+        if ((aux >> 19) & 1) {   // column-window tile: this item's partial through the workspace
+            item_ws_combine<H, Map, PP>(p, acc, slot, it.x, sub, lj, lane);
+            return;
         }
     }
     __syncwarp();   // staging reads done before the area holds the partial
@@ -976,6 +1031,9 @@ struct GProb {
     float* C;
     int m, n, W;
     const int* rowmap;                        // always NULL (hybrid plans are not grouped)
+    const int4* slot_ws;                      // always NULL (column-window tiles are not grouped)
+    float* wsc;
+    int* wsc_counters;
     static constexpr bool kScatter = false;   // no fused all-gather in grouped launches
 };
 struct GroupParams {

@@ -16,7 +16,7 @@ struct Params {
     int ufk = 4;        // B-row loads in flight per sub-warp step (UFk)
     int packed = 0;     // 1: tuned for the packed-record walk (escs_spmm_packed)
     int colf = 0;       // B columns per lane of the vector map (bCols coarsening), 0 = default
-    int tile_order = 0; // 0 auto, 1 panel order, 2 by longest item
+    int tile_order = 0; // 0 auto, 1 panel order, 2 by longest item, 3 column windows
     int nthreads = 0;   // planner threads
     // staged record walk (staged_kernel.cuh): B rows of a CTA's k-range in
     // shared memory.  staged: 0 = auto, 1 = off (record walk gathers from L2),
@@ -49,6 +49,11 @@ struct PlanHost {
     std::vector<int32_t> slot_aux;    // lead | cnt<<8 | active<<16 | tile_sync<<17 | tile_heavy<<18
     std::vector<int32_t> tile_heavy;  // 2 per tile: heavy id (-1), ordinal
     std::vector<int32_t> heavy_info;  // 4 per heavy panel: panel, ws_base, ntiles, 0
+    // column-window tiles (tile_order 3): per slot {ws offset (floats), panel
+    // counter, the panel's item count, the item's ordinal}; counters, ws floats
+    std::vector<int32_t> slot_ws;
+    int n_wsc_counters = 0;
+    int64_t wsc_floats = 0;
     int n_tiles = 0, n_heavy = 0, n_heavy_tiles = 0, n_split_items = 0;
     bool any_sync = false;
     double plan_seconds = 0.0;
@@ -78,6 +83,11 @@ int rec_words(int h);   // record stride in 32-bit words (esc_kernel.cuh RecFmt<
 
 // Pick cta_warps from the item distribution and build the tile schedule.
 void build_tiles(PlanHost& ph, int cta_warps, bool by_length = true);
+// Column-window tiles: tile = item j of W consecutive panels (the same column
+// window of W panels on one SM, so their B rows are re-read from L1); a split
+// panel's items combine through a per-item workspace slot and a per-panel
+// counter (the last item to arrive sums them in item order).
+void build_tiles_cols(PlanHost& ph, int cta_warps, int bcols);
 
 // Device-side view used by the kernels.
 struct DevPlan {
@@ -88,6 +98,9 @@ struct DevPlan {
     const int32_t* item_aux = nullptr;  // int32[n_slots]
     const int32_t* tile_heavy = nullptr;  // int2[n_tiles]
     const int32_t* heavy = nullptr;     // int4[n_heavy]
+    const int32_t* slot_ws = nullptr;   // int4[n_slots] (column-window tiles)
+    float* wsc = nullptr;               // column-window tiles: per-item partials
+    int32_t* wsc_counters = nullptr;
     float* ws = nullptr;                // float[n_heavy_tiles * h * bcols]
     int32_t* counters = nullptr;        // int32[n_heavy]
     int m = 0, k = 0, nnz = 0, bcols = 0, h = 0, n_tiles = 0, cta_warps = 0, variant = 1, ufk = 4, colf = 0;

@@ -112,6 +112,9 @@ kern::KParams make_params(const DevPlan& dp, const float* vals, const float* B, 
     p.n = dp.bcols;
     p.k = dp.k;
     p.rowmap = dp.rowmap;
+    p.slot_ws = reinterpret_cast<const int4*>(dp.slot_ws);
+    p.wsc = dp.wsc;
+    p.wsc_counters = dp.wsc_counters;
     return p;
 }
 
@@ -300,7 +303,7 @@ int launch_group(int n, const DevPlan* const* dps, const float* const* vals,
         if (dp.n_tiles == 0) continue;
         const bool vec = dp.variant == 1 && al16(B[i]) && al16(C[i]);
         kern::GroupFn g = nullptr;
-        if (vec && dp.h == 1 && smem_for(dp, true) <= 32 * 1024)   // no attribute raise for group kernels
+        if (vec && dp.h == 1 && !dp.slot_ws && smem_for(dp, true) <= 32 * 1024)   // no attribute raise for group kernels
             g = kern::get_vec_group(dp.bcols, dp.colf > 0 ? dp.colf : kern::default_colf(dp.bcols),
                                     dp.ufk);
         if (!g) {

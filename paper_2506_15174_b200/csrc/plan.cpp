@@ -332,6 +332,71 @@ void build_tiles(PlanHost& ph, int W, bool by_length) {
     ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
 }
 
+void build_tiles_cols(PlanHost& ph, int W, int bcols) {
+    const int64_t NI = ph.item_panel.size();
+    const int64_t nP = ph.header[7];
+    const int h = ph.header[5];
+    ph.slot_item.clear();
+    ph.slot_aux.clear();
+    ph.tile_heavy.clear();
+    ph.heavy_info.clear();
+    ph.slot_ws.clear();
+    ph.n_heavy = ph.n_heavy_tiles = ph.n_split_items = 0;
+    ph.any_sync = false;
+    ph.n_wsc_counters = 0;
+    ph.wsc_floats = 0;
+    std::vector<int64_t> first(nP + 1, NI);
+    for (int64_t i = NI - 1; i >= 0; i--) first[ph.item_panel[i]] = i;
+    first[nP] = NI;
+    for (int64_t P = nP - 1; P >= 0; P--)
+        if (first[P] > first[P + 1]) first[P] = first[P + 1];
+    // per split panel: a counter and a workspace range of n x h x bcols floats
+    std::vector<int32_t> ctr(nP, -1);
+    std::vector<int64_t> wsb(nP, 0);
+    int64_t maxn = 0;
+    for (int64_t P = 0; P < nP; P++) {
+        const int64_t n = first[P + 1] - first[P];
+        maxn = std::max(maxn, n);
+        if (n > 1) {
+            ctr[P] = ph.n_wsc_counters++;
+            wsb[P] = ph.wsc_floats;
+            ph.wsc_floats += n * (int64_t)h * bcols;
+            ph.n_split_items += (int32_t)n;
+        }
+    }
+    std::vector<int64_t> grp;
+    auto emit = [&]() {
+        for (int k = 0; k < W; k++) {
+            if (k < (int)grp.size()) {
+                const int64_t it = grp[k], P = ph.item_panel[it], n = first[P + 1] - first[P];
+                const int64_t q = it - first[P];
+                ph.slot_item.push_back((int32_t)it);
+                ph.slot_aux.push_back((1 << 16) | (n > 1 ? (1 << 19) : 0));
+                if (wsb[P] + q * h * bcols >= INT32_MAX) throw std::runtime_error("column-window workspace too large");
+                ph.slot_ws.insert(ph.slot_ws.end(), {(int32_t)(wsb[P] + q * h * bcols), ctr[P], (int32_t)n, (int32_t)q});
+            } else {
+                ph.slot_item.push_back(-1);
+                ph.slot_aux.push_back(0);
+                ph.slot_ws.insert(ph.slot_ws.end(), {0, -1, 0, 0});
+            }
+        }
+        ph.tile_heavy.push_back(-1);
+        ph.tile_heavy.push_back(0);
+        grp.clear();
+    };
+    // item index j of consecutive panels, j-major: the tiles of one column
+    // window are launched together
+    for (int64_t j = 0; j < maxn; j++) {
+        for (int64_t P = 0; P < nP; P++) {
+            if (first[P + 1] - first[P] <= j) continue;
+            grp.push_back(first[P] + j);
+            if ((int)grp.size() == W) emit();
+        }
+        if (!grp.empty()) emit();
+    }
+    ph.n_tiles = (int)(ph.tile_heavy.size() / 2);
+}
+
 int rec_words(int h) { return h == 1 ? 2 : (h <= 3 ? 4 : (h <= 7 ? 8 : 12)); }
 
 // The staged walk's schedule.  Row block rb = panels [rb*nslot, (rb+1)*nslot)

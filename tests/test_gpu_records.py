@@ -176,3 +176,32 @@ def test_packed_rejects_scalar_and_misaligned(torch_cuda):
     with pytest.raises(escs.EscsError) as e:
         escs.escs_spmm_packed(pl, pk, dB, C)
     assert e.value.code == escs.ESCS_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("packed", [1, 0])
+@pytest.mark.parametrize("n,T,W", [(128, 60, 12), (64, 17, 4), (32, 300, 16), (128, 1000, 8)])
+def test_column_window_tiles_exact(torch_cuda, packed, n, T, W):
+    """tile_order 3 (column windows: item j of W panels per CTA, split panels
+    combined through per-item workspace slots and a per-panel counter): exact
+    on the dyadic twin, bitwise stable across repeated calls (counters reset),
+    ragged m, empty rows, panels with one item and with many."""
+    from paper_2506_15174_b200 import escs
+    A = synth.random_csr(333, 2000, 60000, 13, empty_rows=(0, 7, 332), dense_rows=(5,))
+    Ad, Bd = synth.dyadic_twin(A, n, 9)
+    pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, n, ufi=1, T=T, cta_warps=W, tile_order=3,
+                           packed=packed)
+    assert pl.info["tile_order"] == 3
+    dv = torch_cuda.from_numpy(Ad.vals).cuda()
+    dB = torch_cuda.from_numpy(Bd).cuda()
+    pk = escs.escs_pack(pl, dv) if packed else None
+    outs = []
+    for _ in range(3):
+        C = torch_cuda.full((A.m, n), float("nan"), device="cuda")
+        if packed:
+            escs.escs_spmm_packed(pl, pk, dB, C)
+        else:
+            escs.escs_spmm(pl, dv, dB, C)
+        torch_cuda.cuda.synchronize()
+        outs.append(C.cpu().numpy())
+    check_exact(Ad, Bd, outs[0])
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
