@@ -178,8 +178,8 @@ def test_tuning_cache_reuses_parameters(torch_cuda, monkeypatch):
     with the first one's tuned parameters (autotuned = 2), and is exact."""
     from paper_2506_15174_b200 import escs
     monkeypatch.delenv("ESCS_TUNE_CACHE", raising=False)
-    A1 = synth.magnitude_pruned(384, 768, 0.8, 501)
-    A2 = synth.magnitude_pruned(384, 768, 0.8, 502)
+    A1 = synth.magnitude_pruned(389, 771, 0.8, 501)   # a shape no other test tunes
+    A2 = synth.magnitude_pruned(389, 771, 0.8, 502)
     assert A1.nnz == A2.nnz
     p1 = escs.escs_plan_ex(A1.m, A1.k, A1.nnz, A1.rowptr, A1.colidx, 64, packed=1, autotune=1, tile_order=1)
     p2 = escs.escs_plan_ex(A2.m, A2.k, A2.nnz, A2.rowptr, A2.colidx, 64, packed=1, autotune=1, tile_order=1)
