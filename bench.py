@@ -975,6 +975,13 @@ def run_escs(args):
             "roofline": {
                 "bound": "hbm", "achieved": dom_gbs, "peak": hbm, "unit": "GB/s", "frac": dom_gbs / hbm,
                 "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_breakdown": {
+                    "record_stream_bytes": 4 * int(dinf["packed_words"]),
+                    "b_bytes": 4 * pd.A.k * pd.bcols, "c_bytes": 4 * pd.A.m * pd.bcols,
+                    "what": ("bytes the launch must read or write once: the plan's record stream (escs_pack: "
+                             "one record per gcol; UFi > 1 records store a value slot for every pattern row, 0.0 "
+                             "for the absent ones, Reading R20 -- UFi 8: 48 bytes per record), B and C; "
+                             "`traffic` above this is re-reads, below it is L2 hits")},
                 "kernel": f"{'esc_staged_kernel' if dinf['staged'] else 'esc_rec_kernel' if dinf['packed'] else 'esc_spmm_kernel'} "
                           f"on the dominant layer {pd.name}",
                 "achieved_how": ("compulsory bytes (8*nnz + 4*(m+1) + 4*k*bCols + 4*m*bCols, SURVEY 8(d)) of the "
