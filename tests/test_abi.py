@@ -112,14 +112,14 @@ def test_params_out_of_range_rejected():
     import pytest
     from paper_2506_15174_b200 import escs, synth
     A = synth.random_csr(20, 30, 100, 1)
-    for bad in ({"colf": 5}, {"tile_order": 3}, {"cta_warps": 17}, {"variant": 3},
+    for bad in ({"colf": 5}, {"tile_order": 4}, {"cta_warps": 17}, {"variant": 3},
                 {"autotune": 3}, {"autotune": -1}):
         with pytest.raises(escs.EscsError) as e:
             escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **bad)
         assert e.value.code == escs.ESCS_ERR_ARG
-    for ok in ({"colf": 8}, {"tile_order": 2}, {"tile_order": 1}):
+    for ok in ({"colf": 8}, {"tile_order": 2}, {"tile_order": 1}, {"tile_order": 3}):
         pl = escs.escs_plan_ex(A.m, A.k, A.nnz, A.rowptr, A.colidx, 32, host_only=1, **ok)
-        assert pl.info["tile_order"] in (1, 2)
+        assert pl.info["tile_order"] == ok.get("tile_order", pl.info["tile_order"]) and pl.info["tile_order"] in (1, 2, 3)
         pl.close()
 
 
