@@ -69,7 +69,11 @@ def main():
                 except escs.EscsError as ex:
                     print(f"  {name} h{h} W{W} npw{npw} ns{ns}: {ex}", flush=True)
                     continue
-                t, err = run(pl)
+                try:
+                    t, err = run(pl)
+                except escs.EscsError as ex:
+                    print(f"  {name} h{h} W{W} npw{npw}: {ex}", flush=True)
+                    continue
                 print(f"  {name} h{h} W{W} npw{npw} ns{pl.info['st_nsplit']} kb{pl.info['st_kb']} F{pl.info['colf']} ctas {pl.info['st_ctas']} L{pl.info['st_launches']} "
                       f"{t*1e3:7.2f} us err {err:.1e}", flush=True)
                 res.append({"case": name, "h": h, "warps": W, "npw": npw, "nsplit": ns, "us": t * 1e3, "err": err})
