@@ -1102,7 +1102,7 @@ def main(argv=None):
                     help="plan with the parameter table only (default: plan-time autotuning)")
     ap.add_argument("--shard", default="auto", choices=["auto", "rows", "problems"],
                     help="N>1: partition a suite by problems or row-block shard every problem")
-    ap.add_argument("--e2e-chunks", type=int, default=8,
+    ap.add_argument("--e2e-chunks", type=int, default=16,
                     help="e2e: copy/compute pipeline depth (chunks of layers per step)")
     ap.add_argument("--allgather", action="store_true",
                     help="N>1: also time the optional NCCL all-gather of C (not on the hot path)")
