@@ -797,12 +797,13 @@ def run_escs(args):
                 h_out[lo:hi].copy_(d_out[lo:hi], non_blocking=True)
         stream.wait_stream(out_s)
 
-    if nprob == 1 and args.e2e_chunks > 1 and shard_problems[0][1]["A"].m >= 8 * args.e2e_chunks:
+    E1 = min(args.e2e_chunks, 8)   # one large problem: at most 8 row blocks (each its own plan)
+    if nprob == 1 and E1 > 1 and shard_problems[0][1]["A"].m >= 8 * E1:
         # one large problem: B in, then row blocks (one plan per block, built
         # and packed once) computed while earlier blocks' C rows go back
         p0, d0 = shard_problems[0]
         A0, n0 = d0["A"], p0.bcols
-        E = args.e2e_chunks
+        E = E1
         blocks = []
         for r in range(E):
             r0, r1 = synth.shard_bounds(A0.m, E, r)
